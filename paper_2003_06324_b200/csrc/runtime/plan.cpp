@@ -1,0 +1,518 @@
+// Runtime: compiles, caches and launches lowered strategies on the B200.
+//   generic plans  -> emitted CUDA -> NVRTC (sm_100a, --fmad=false) -> cubin
+//                     (memory + on-disk cache keyed by source/options) -> cuModule
+//   tcgen05 plans  -> the AOT tensor-core kernel family (sm100/gemm.cu)
+// NVRTC and the driver API are resolved at run time (dlopen / driver entry
+// points) so the library loads on hosts without a GPU.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <sys/stat.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+
+#include "../sm100/tc_gemm.hpp"
+#include "fireiron/backend.hpp"
+
+namespace fireiron {
+
+long generic_shared_bytes(const Program& prog);
+namespace rt {
+cudaError_t convert_f32(const float* src, void* dst, int64_t n, int elem, cudaStream_t s);
+cudaError_t widen_to_f32(const void* src, float* dst, int64_t n, int elem, cudaStream_t s);
+int device_sm_count();
+}  // namespace rt
+
+namespace {
+
+[[noreturn]] void cuda_fail(const std::string& what, cudaError_t e) {
+    throw BackendError(100, what + ": " + cudaGetErrorString(e));
+}
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) cuda_fail(what, e);
+}
+
+// ---------------------------------------------------------------- NVRTC
+struct Nvrtc {
+    using Prog = void*;
+    int (*create)(Prog*, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+    int (*compile)(Prog, int, const char* const*) = nullptr;
+    int (*log_size)(Prog, size_t*) = nullptr;
+    int (*log)(Prog, char*) = nullptr;
+    int (*cubin_size)(Prog, size_t*) = nullptr;
+    int (*cubin)(Prog, char*) = nullptr;
+    int (*destroy)(Prog*) = nullptr;
+    int (*version)(int*, int*) = nullptr;
+    bool ok = false;
+    std::string error;
+
+    static const Nvrtc& get() {
+        static Nvrtc n = [] {
+            Nvrtc x;
+            void* h = nullptr;
+            for (const char* p : {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"})
+                if ((h = dlopen(p, RTLD_NOW | RTLD_GLOBAL))) break;
+            if (!h) {
+                x.error = "libnvrtc.so.12 not found";
+                return x;
+            }
+            auto sym = [&](const char* s) { return dlsym(h, s); };
+            x.create = reinterpret_cast<decltype(x.create)>(sym("nvrtcCreateProgram"));
+            x.compile = reinterpret_cast<decltype(x.compile)>(sym("nvrtcCompileProgram"));
+            x.log_size = reinterpret_cast<decltype(x.log_size)>(sym("nvrtcGetProgramLogSize"));
+            x.log = reinterpret_cast<decltype(x.log)>(sym("nvrtcGetProgramLog"));
+            x.cubin_size = reinterpret_cast<decltype(x.cubin_size)>(sym("nvrtcGetCUBINSize"));
+            x.cubin = reinterpret_cast<decltype(x.cubin)>(sym("nvrtcGetCUBIN"));
+            x.destroy = reinterpret_cast<decltype(x.destroy)>(sym("nvrtcDestroyProgram"));
+            x.version = reinterpret_cast<decltype(x.version)>(sym("nvrtcVersion"));
+            x.ok = x.create && x.compile && x.log_size && x.log && x.cubin_size && x.cubin && x.destroy;
+            if (!x.ok) x.error = "libnvrtc is missing required symbols";
+            return x;
+        }();
+        return n;
+    }
+};
+
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+std::string cache_dir() {
+    if (const char* e = std::getenv("FI_KERNEL_CACHE")) return e;
+    const char* home = std::getenv("HOME");
+    return std::string(home ? home : "/tmp") + "/.cache/fireiron_b200";
+}
+
+void mkdirs(const std::string& path) {
+    std::string cur;
+    for (size_t i = 0; i < path.size(); ++i) {
+        cur += path[i];
+        if (path[i] == '/' && cur.size() > 1) mkdir(cur.c_str(), 0755);
+    }
+    mkdir(path.c_str(), 0755);
+}
+
+// source -> cubin (sm_100a), memoised in process and on disk
+std::string compile_cubin(const std::string& source, const std::string& name) {
+    static std::mutex mu;
+    static std::map<uint64_t, std::string> memo;
+    const std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "--fmad=false", "-std=c++17",
+                                           "-default-device", "-lineinfo",
+                                           "--include-path=/usr/local/cuda/include"};
+    std::string key_text = source;
+    for (const auto& o : opts) key_text += "\n" + o;
+    const uint64_t key = fnv1a(key_text);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        if (auto it = memo.find(key); it != memo.end()) return it->second;
+    }
+    char hex[32];
+    std::snprintf(hex, sizeof(hex), "%016llx", static_cast<unsigned long long>(key));
+    const std::string path = cache_dir() + "/" + hex + ".cubin";
+    {
+        std::ifstream in(path, std::ios::binary);
+        if (in) {
+            std::ostringstream ss;
+            ss << in.rdbuf();
+            std::string bin = ss.str();
+            if (!bin.empty()) {
+                std::lock_guard<std::mutex> g(mu);
+                memo[key] = bin;
+                return bin;
+            }
+        }
+    }
+    const Nvrtc& nv = Nvrtc::get();
+    if (!nv.ok) throw BackendError(101, "NVRTC unavailable: " + nv.error);
+    Nvrtc::Prog p = nullptr;
+    if (nv.create(&p, source.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr) != 0)
+        throw BackendError(101, "nvrtcCreateProgram failed");
+    std::vector<const char*> argv;
+    for (const auto& o : opts) argv.push_back(o.c_str());
+    const int rc = nv.compile(p, static_cast<int>(argv.size()), argv.data());
+    if (rc != 0) {
+        size_t n = 0;
+        nv.log_size(p, &n);
+        std::string log(n, '\0');
+        nv.log(p, log.data());
+        nv.destroy(&p);
+        throw BackendError(101, "NVRTC compilation of " + name + " failed:\n" + log);
+    }
+    size_t n = 0;
+    nv.cubin_size(p, &n);
+    std::string bin(n, '\0');
+    nv.cubin(p, bin.data());
+    nv.destroy(&p);
+    mkdirs(cache_dir());
+    {
+        const std::string tmp = path + ".tmp" + std::to_string(getpid());
+        std::ofstream out(tmp, std::ios::binary);
+        out.write(bin.data(), static_cast<std::streamsize>(bin.size()));
+        out.close();
+        std::rename(tmp.c_str(), path.c_str());
+    }
+    std::lock_guard<std::mutex> g(mu);
+    memo[key] = bin;
+    return bin;
+}
+
+// ---------------------------------------------------------------- driver API
+struct Driver {
+    CUresult (*module_load_data)(CUmodule*, const void*) = nullptr;
+    CUresult (*module_get_function)(CUfunction*, CUmodule, const char*) = nullptr;
+    CUresult (*module_unload)(CUmodule) = nullptr;
+    CUresult (*func_set_attribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+    CUresult (*launch_kernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                              CUstream, void**, void**) = nullptr;
+    CUresult (*get_error_string)(CUresult, const char**) = nullptr;
+
+    static const Driver& get() {
+        static Driver d = [] {
+            Driver x;
+            auto sym = [](const char* s) -> void* {
+                void* p = nullptr;
+                cudaDriverEntryPointQueryResult q;
+                if (cudaGetDriverEntryPoint(s, &p, cudaEnableDefault, &q) != cudaSuccess ||
+                    q != cudaDriverEntryPointSuccess)
+                    return nullptr;
+                return p;
+            };
+            x.module_load_data = reinterpret_cast<decltype(x.module_load_data)>(sym("cuModuleLoadData"));
+            x.module_get_function = reinterpret_cast<decltype(x.module_get_function)>(sym("cuModuleGetFunction"));
+            x.module_unload = reinterpret_cast<decltype(x.module_unload)>(sym("cuModuleUnload"));
+            x.func_set_attribute = reinterpret_cast<decltype(x.func_set_attribute)>(sym("cuFuncSetAttribute"));
+            x.launch_kernel = reinterpret_cast<decltype(x.launch_kernel)>(sym("cuLaunchKernel"));
+            x.get_error_string = reinterpret_cast<decltype(x.get_error_string)>(sym("cuGetErrorString"));
+            return x;
+        }();
+        if (!d.module_load_data || !d.launch_kernel) throw BackendError(100, "CUDA driver entry points unavailable");
+        return d;
+    }
+    void check(CUresult r, const char* what) const {
+        if (r == CUDA_SUCCESS) return;
+        const char* s = "unknown";
+        if (get_error_string) get_error_string(r, &s);
+        throw BackendError(100, std::string(what) + ": " + s);
+    }
+};
+
+int elem_code(ElemType e) { return e == ElemType::F32 ? 0 : e == ElemType::F16 ? 1 : 2; }
+
+bool reads_buffer(const StmtList& body, int id) {
+    for (const auto& s : body) {
+        if (const auto* l = std::get_if<LoopStmt>(&s.v)) {
+            if (reads_buffer(l->body, id)) return true;
+        } else if (const auto* f = std::get_if<FmaStmt>(&s.v)) {
+            if (f->c.buf == id || f->a.buf == id || f->b.buf == id) return true;
+        } else if (const auto* c = std::get_if<CopyStmt>(&s.v)) {
+            if (c->src.buf == id) return true;
+        } else if (const auto* w = std::get_if<WmmaLoadStmt>(&s.v)) {
+            if (w->src.buf == id) return true;
+        } else if (const auto* m = std::get_if<MicroKernelStmt>(&s.v)) {
+            for (const auto& o : m->operands)
+                if (o.second.buf == id) return true;
+        }
+    }
+    return false;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- Plan
+struct Plan::Impl {
+    Program prog;
+    MicroKernelSet mks;  // owned copy (the Program's micro-kernel pointers index it)
+    PlanInfo info;
+    std::string source;
+    int device = 0;
+    // generic
+    CUmodule module = nullptr;
+    CUfunction func = nullptr;
+    long smem = 0;
+    bool zero_c = false;
+    // tcgen05
+    sm100::TcGemmConfig tc;
+    sm100::TcGemmProblem tp;
+    int32_t* d_tile_order = nullptr;
+    // run_host scratch
+    mutable std::mutex mu;
+    mutable void* scratch = nullptr;
+    mutable size_t scratch_bytes = 0;
+    mutable cudaStream_t own_stream = nullptr;
+
+    ~Impl() {
+        if (module) {
+            try {
+                Driver::get().module_unload(module);
+            } catch (...) {
+            }
+        }
+        if (d_tile_order) cudaFree(d_tile_order);
+        if (scratch) cudaFree(scratch);
+        if (own_stream) cudaStreamDestroy(own_stream);
+    }
+
+    const BufferDecl& root(int i) const { return prog.plan.at(i); }
+    int out_root() const { return prog.root.is_matmul() ? 2 : 1; }
+};
+
+Plan::Plan(std::unique_ptr<Impl> impl) : impl_(std::move(impl)) {}
+Plan::~Plan() = default;
+const PlanInfo& Plan::info() const { return impl_->info; }
+const Program& Plan::program() const { return impl_->prog; }
+const std::string& Plan::source() const { return impl_->source; }
+
+std::shared_ptr<Plan> Plan::from_script(const std::string& script, long m, long n, long k, int device) {
+    ParsedScript ps = parse_script(script);
+    apply_size_overrides(ps, m, n, k);
+    return create(ps.root, ps.tree, ps.micro_kernels, device);
+}
+
+std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const MicroKernelSet& mks, int device) {
+    auto impl = std::make_unique<Impl>();
+    impl->mks = mks;
+    impl->device = device;
+    impl->prog = lower(root, tree, impl->mks);  // throws on invalid trees
+    Program& prog = impl->prog;
+    PlanInfo& info = impl->info;
+    info.grid_x = prog.launch.grid_x;
+    info.grid_y = prog.launch.grid_y;
+    info.block_threads = prog.launch.block_threads;
+    info.entry_name = prog.entry_name;
+    info.flops = root.is_matmul() ? 2.0 * static_cast<double>(root.m()) * root.n() * root.k() : 0.0;
+
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaFree(nullptr), "CUDA context initialisation");
+
+    if (prog.uses_hmma)
+        throw BackendError(103, "HMMA.884.F16.TN is a Volta quad-pair leaf with no defined thread "
+                                "semantics in the reference (sim.hpp:436-437); bind UMMA on sm_100a");
+    if (prog.uses_tcgen05) {
+        TcStrategy tc = match_tc_strategy(root, tree, impl->mks);
+        if (!tc.matched) throw BackendError(103, "tensor-core tree has no sm_100a lowering: " + tc.why_not);
+        const auto& mm = root.mm();
+        sm100::TcGemmConfig& c = impl->tc;
+        c.cta_group = tc.cta_group;
+        c.bn = tc.tile_n;
+        c.split_k = tc.split_k;
+        c.ab_format = mm.a.elem == ElemType::BF16 ? 1 : 0;
+        c.a_mn_major = mm.a.layout.major == Major::ColMajor ? 1 : 0;
+        c.b_mn_major = mm.b.layout.major == Major::RowMajor ? 1 : 0;
+        c.c_row_major = mm.c.layout.major == Major::RowMajor ? 1 : 0;
+        c.out_type = elem_code(mm.c.elem);
+        c.group_m = 8;
+        c.stages = tc.stages;
+        if (sm100::tc_gemm_check(c, static_cast<int>(root.m()), static_cast<int>(root.n()),
+                                 static_cast<int>(root.k())) != sm100::kTcOk)
+            throw BackendError(103, "no tcgen05 kernel instance for this tile configuration");
+        sm100::TcGemmProblem& p = impl->tp;
+        p.M = static_cast<int>(root.m());
+        p.N = static_cast<int>(root.n());
+        p.K = static_cast<int>(root.k());
+        p.lda = mm.a.layout.leading_dim(mm.a.rows, mm.a.cols);
+        p.ldb = mm.b.layout.leading_dim(mm.b.rows, mm.b.cols);
+        p.ldc = mm.c.layout.leading_dim(mm.c.rows, mm.c.cols);
+        if ((p.lda * 2) % 16 || (p.ldb * 2) % 16)
+            throw BackendError(103, "TMA needs 16-byte aligned operand strides (leading dim % 8)");
+        p.num_sms = rt::device_sm_count();
+        if (!tc.tile_order.empty()) {
+            ck(cudaMalloc(&impl->d_tile_order, tc.tile_order.size() * sizeof(int32_t)), "cudaMalloc");
+            ck(cudaMemcpy(impl->d_tile_order, tc.tile_order.data(), tc.tile_order.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+            p.tile_order = impl->d_tile_order;
+        }
+        info.kind = 1;
+        info.cta_group = tc.cta_group;
+        info.tile_m = tc.tile_m;
+        info.tile_n = tc.tile_n;
+        info.split_k = tc.split_k;
+        info.cluster = tc.cta_group * tc.split_k;
+        info.stages = sm100::tc_gemm_stages(c);
+        info.tmem_cols = sm100::tc_gemm_tmem_cols(c);
+        info.shared_bytes = sm100::tc_gemm_smem_bytes(c);
+        const long tiles = (root.m() / tc.tile_m) * (root.n() / tc.tile_n);
+        const long clusters = std::min<long>(tiles, p.num_sms / info.cluster);
+        info.launch_ctas = clusters * info.cluster;
+        impl->source = generate(prog).source;
+        return std::shared_ptr<Plan>(new Plan(std::move(impl)));
+    }
+
+    // generic: emit -> NVRTC -> module
+    impl->source = generate(prog).source;
+    impl->smem = generic_shared_bytes(prog);
+    const std::string cubin = compile_cubin(impl->source, prog.entry_name);
+    const Driver& drv = Driver::get();
+    drv.check(drv.module_load_data(&impl->module, cubin.data()), "cuModuleLoadData");
+    drv.check(drv.module_get_function(&impl->func, impl->module, prog.entry_name.c_str()), "cuModuleGetFunction");
+    if (impl->smem > 48 * 1024)
+        drv.check(drv.func_set_attribute(impl->func, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                         static_cast<int>(impl->smem)),
+                  "cuFuncSetAttribute");
+    impl->zero_c = reads_buffer(prog.body, impl->out_root());
+    info.kind = 0;
+    info.shared_bytes = impl->smem;
+    info.launch_ctas = prog.launch.grid_x * prog.launch.grid_y;
+    return std::shared_ptr<Plan>(new Plan(std::move(impl)));
+}
+
+void Plan::launch(const void* dA, const void* dB, void* dC, void* stream) const {
+    const Impl& I = *impl_;
+    auto s = static_cast<cudaStream_t>(stream);
+    if (I.info.kind == 1) {
+        sm100::TcGemmProblem p = I.tp;
+        p.A = dA;
+        p.B = dB;
+        p.C = dC;
+        if ((reinterpret_cast<uintptr_t>(dA) | reinterpret_cast<uintptr_t>(dB)) & 15)
+            throw BackendError(104, "TMA operands must be 16-byte aligned");
+        const int r = sm100::tc_gemm_launch(I.tc, p, s);
+        if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+        return;
+    }
+    const BufferDecl& out = I.root(I.out_root());
+    if (I.zero_c) ck(cudaMemsetAsync(dC, 0, static_cast<size_t>(out.extent()) * byte_width(out.elem), s), "cudaMemsetAsync");
+    void* args[3];
+    const void* a = dA;
+    const void* b = dB;
+    void* c = dC;
+    int nargs = 0;
+    if (I.prog.root.is_matmul()) {
+        args[0] = &a;
+        args[1] = &b;
+        args[2] = &c;
+        nargs = 3;
+    } else {
+        args[0] = &a;
+        args[1] = &c;
+        nargs = 2;
+    }
+    (void)nargs;
+    const Driver& drv = Driver::get();
+    drv.check(drv.launch_kernel(I.func, static_cast<unsigned>(I.prog.launch.grid_x),
+                                static_cast<unsigned>(I.prog.launch.grid_y), 1,
+                                static_cast<unsigned>(std::max<long>(1, I.prog.launch.block_threads)), 1, 1,
+                                static_cast<unsigned>(I.smem), reinterpret_cast<CUstream>(s), args, nullptr),
+              "cuLaunchKernel");
+}
+
+RunResult Plan::run_host(const Matrix& a, const Matrix* b, void* stream) const {
+    const Impl& I = *impl_;
+    const Spec& root = I.prog.root;
+    std::lock_guard<std::mutex> g(I.mu);
+    ck(cudaSetDevice(I.device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!s) {
+        if (!I.own_stream) ck(cudaStreamCreateWithFlags(&I.own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        s = I.own_stream;
+    }
+    const int nin = root.is_matmul() ? 2 : 1;
+    const Matrix* ins[2] = {&a, b};
+    if (root.is_matmul() && !b) fail(ErrorKind::ShapeMismatch, "matmul execution needs both A and B inputs");
+    for (int i = 0; i < nin; ++i) {
+        const BufferDecl& r = I.root(i);
+        if (ins[i]->rows != r.rows || ins[i]->cols != r.cols)
+            fail(ErrorKind::ShapeMismatch, "input for " + r.name + " must be " + std::to_string(r.rows) + "x" +
+                                               std::to_string(r.cols));
+    }
+    const BufferDecl& out = I.root(I.out_root());
+    // scratch layout: [f32 staging of each input][typed inputs][typed C][f32 C]
+    auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+    size_t off = 0;
+    size_t f32_in[2] = {0, 0}, typed_in[2] = {0, 0};
+    for (int i = 0; i < nin; ++i) {
+        f32_in[i] = off;
+        off = align(off + static_cast<size_t>(I.root(i).extent()) * 4);
+    }
+    for (int i = 0; i < nin; ++i) {
+        typed_in[i] = off;
+        off = align(off + static_cast<size_t>(I.root(i).extent()) * byte_width(I.root(i).elem));
+    }
+    const size_t typed_c = off;
+    off = align(off + static_cast<size_t>(out.extent()) * byte_width(out.elem));
+    const size_t f32_c = off;
+    off = align(off + static_cast<size_t>(out.extent()) * 4);
+    if (I.scratch_bytes < off) {
+        if (I.scratch) cudaFree(I.scratch);
+        I.scratch = nullptr;
+        ck(cudaMalloc(&I.scratch, off), "cudaMalloc");
+        I.scratch_bytes = off;
+    }
+    auto* base = static_cast<char*>(I.scratch);
+    for (int i = 0; i < nin; ++i) {
+        // the host Matrix stores the root's physical layout; pads carry zeros
+        const BufferDecl& r = I.root(i);
+        if (static_cast<long>(ins[i]->data.size()) != r.extent() || !(ins[i]->layout == r.layout)) {
+            Matrix tmp = Matrix::zeros(r.rows, r.cols, r.layout);
+            for (long rr = 0; rr < r.rows; ++rr)
+                for (long cc = 0; cc < r.cols; ++cc) tmp.at(rr, cc) = ins[i]->at(rr, cc);
+            ck(cudaMemcpyAsync(base + f32_in[i], tmp.data.data(), tmp.data.size() * 4, cudaMemcpyHostToDevice, s),
+               "cudaMemcpyAsync");
+            ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        } else {
+            ck(cudaMemcpyAsync(base + f32_in[i], ins[i]->data.data(), ins[i]->data.size() * 4,
+                               cudaMemcpyHostToDevice, s),
+               "cudaMemcpyAsync");
+        }
+        ck(rt::convert_f32(reinterpret_cast<float*>(base + f32_in[i]), base + typed_in[i], r.extent(),
+                           elem_code(r.elem), s),
+           "input conversion");
+    }
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "cudaEventCreate");
+    ck(cudaEventCreate(&e1), "cudaEventCreate");
+    ck(cudaEventRecord(e0, s), "cudaEventRecord");
+    launch(base + typed_in[0], nin > 1 ? base + typed_in[1] : nullptr, base + typed_c, s);
+    ck(cudaEventRecord(e1, s), "cudaEventRecord");
+    ck(rt::widen_to_f32(base + typed_c, reinterpret_cast<float*>(base + f32_c), out.extent(), elem_code(out.elem), s),
+       "output conversion");
+    RunResult res;
+    res.output = Matrix::zeros(out.rows, out.cols, out.layout);
+    ck(cudaMemcpyAsync(res.output.data.data(), base + f32_c, static_cast<size_t>(out.extent()) * 4,
+                       cudaMemcpyDeviceToHost, s),
+       "cudaMemcpyAsync");
+    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    res.device_ms = ms;
+    return res;
+}
+
+// ---------------------------------------------------------------- run (drop-in)
+namespace {
+void collect_micro_kernels(const StmtList& body, MicroKernelSet& mks) {
+    for (const auto& s : body) {
+        if (const auto* l = std::get_if<LoopStmt>(&s.v)) collect_micro_kernels(l->body, mks);
+        if (const auto* m = std::get_if<MicroKernelStmt>(&s.v))
+            if (m->mk && !mks.find(m->mk->name)) mks.register_kernel(*m->mk);
+    }
+}
+}  // namespace
+
+RunResult run(const Program& prog, const Matrix& a, const Matrix* b, RunOptions opts) {
+    if (!prog.tree) fail(ErrorKind::InvalidTree, "program carries no strategy tree (build it with lower())");
+    MicroKernelSet mks;
+    collect_micro_kernels(prog.body, mks);
+    auto plan = Plan::create(prog.root, prog.tree, mks, opts.device);
+    return plan->run_host(a, b, opts.stream);
+}
+
+RunResult run(const Spec& root, const NodePtr& tree, const Matrix& a, const Matrix* b, RunOptions opts,
+              const MicroKernelSet& mks) {
+    auto plan = Plan::create(root, tree, mks, opts.device);
+    return plan->run_host(a, b, opts.stream);
+}
+
+}  // namespace fireiron

@@ -1,0 +1,183 @@
+// Host side of the tcgen05 GEMM family: TMA descriptor encoding, kernel
+// selection by (cta_group, BN, split-K) and cluster launch.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "gemm_kernel.cuh"
+#include "tc_gemm.hpp"
+
+namespace fireiron::sm100 {
+
+namespace {
+
+// The driver entry point is resolved through the runtime so the library loads
+// (and its IR services work) on hosts without libcuda.so.1.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<EncodeTiledFn>(nullptr);
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+CUresult encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t d0,
+                   uint64_t d1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1) {
+    EncodeTiledFn encode = encode_tiled_fn();
+    if (!encode) return CUDA_ERROR_NOT_INITIALIZED;
+    cuuint64_t dims[2] = {d0, d1};
+    cuuint64_t strides[1] = {stride1_bytes};
+    cuuint32_t box[2] = {box0, box1};
+    cuuint32_t estr[2] = {1, 1};
+    return encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+template <int kCtaGroup, int BN, int kSplitK>
+int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream) {
+    using S = GemmShape<kCtaGroup, BN, kSplitK>;
+    auto kernel = fi_sm100_gemm<kCtaGroup, BN, kSplitK>;
+    constexpr int kCluster = kCtaGroup * kSplitK;
+
+    const CUtensorMapDataType dt =
+        cfg.ab_format == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    CUtensorMap tmA, tmB;
+    CUresult r;
+    if (cfg.a_mn_major)
+        r = encode_2d(&tmA, dt, p.A, p.M, p.K, static_cast<uint64_t>(p.lda) * 2, 64, 64);
+    else
+        r = encode_2d(&tmA, dt, p.A, p.K, p.M, static_cast<uint64_t>(p.lda) * 2, 64, S::BM);
+    if (r != CUDA_SUCCESS) return kTcErrTensorMap;
+    if (cfg.b_mn_major)
+        r = encode_2d(&tmB, dt, p.B, p.N, p.K, static_cast<uint64_t>(p.ldb) * 2, 64, 64);
+    else
+        r = encode_2d(&tmB, dt, p.B, p.K, p.N, static_cast<uint64_t>(p.ldb) * 2, 64, S::BN_LOCAL);
+    if (r != CUDA_SUCCESS) return kTcErrTensorMap;
+
+    GemmArgs args;
+    args.C = p.C;
+    args.ldc = p.ldc;
+    args.M = p.M;
+    args.N = p.N;
+    args.K = p.K;
+    args.tiles_m = p.M / S::BM_TILE;
+    args.tiles_n = p.N / BN;
+    args.k_blocks = p.K / S::BK / kSplitK;
+    args.ab_format = cfg.ab_format;
+    args.a_mn_major = cfg.a_mn_major;
+    args.b_mn_major = cfg.b_mn_major;
+    args.c_row_major = cfg.c_row_major;
+    args.out_type = cfg.out_type;
+    args.group_m = cfg.group_m > 0 ? cfg.group_m : 8;
+    args.tile_order = p.tile_order;
+    args.stages = cfg.stages;
+
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [&] {
+        attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        S::SMEM_BYTES);
+        if (attr_err == cudaSuccess && kCluster > 8)
+            attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    });
+    if (attr_err != cudaSuccess) return kTcErrCuda;
+
+    const int tiles = args.tiles_m * args.tiles_n;
+    int sms = p.num_sms > 0 ? p.num_sms : 148;
+    int clusters = sms / kCluster;
+    if (p.max_ctas > 0 && p.max_ctas / kCluster < clusters) clusters = p.max_ctas / kCluster;
+    if (clusters > tiles) clusters = tiles;
+    if (clusters < 1) clusters = 1;
+
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(clusters * kCluster, 1, 1);
+    lc.blockDim = dim3(S::kThreads, 1, 1);
+    lc.dynamicSmemBytes = S::SMEM_BYTES;
+    lc.stream = stream;
+    cudaLaunchAttribute attrs[1];
+    int nattr = 0;
+    if (kCluster > 1) {
+        attrs[0].id = cudaLaunchAttributeClusterDimension;
+        attrs[0].val.clusterDim.x = kCluster;
+        attrs[0].val.clusterDim.y = 1;
+        attrs[0].val.clusterDim.z = 1;
+        nattr = 1;
+    }
+    lc.attrs = attrs;
+    lc.numAttrs = nattr;
+    cudaError_t e = cudaLaunchKernelEx(&lc, kernel, tmA, tmB, args);
+    return e == cudaSuccess ? kTcOk : kTcErrCuda;
+}
+
+}  // namespace
+
+int tc_gemm_stages(const TcGemmConfig& c) {
+#define FI_STAGES(CG, BN, SK)                                          \
+    if (c.cta_group == CG && c.bn == BN && c.split_k == SK) {          \
+        const int mx = GemmShape<CG, BN, SK>::kStages;                 \
+        return (c.stages > 0 && c.stages < mx) ? c.stages : mx;        \
+    }
+    FI_STAGES(1, 64, 1) FI_STAGES(1, 128, 1) FI_STAGES(1, 256, 1)
+    FI_STAGES(2, 128, 1) FI_STAGES(2, 256, 1)
+    FI_STAGES(1, 64, 2) FI_STAGES(1, 128, 2) FI_STAGES(1, 128, 4) FI_STAGES(1, 256, 2) FI_STAGES(1, 256, 4) FI_STAGES(2, 256, 2) FI_STAGES(2, 256, 4) FI_STAGES(2, 128, 2) FI_STAGES(2, 128, 4)
+#undef FI_STAGES
+    return 0;
+}
+
+int tc_gemm_smem_bytes(const TcGemmConfig& c) {
+#define FI_SMEM(CG, BN, SK) \
+    if (c.cta_group == CG && c.bn == BN && c.split_k == SK) return GemmShape<CG, BN, SK>::SMEM_BYTES;
+    FI_SMEM(1, 64, 1) FI_SMEM(1, 128, 1) FI_SMEM(1, 256, 1)
+    FI_SMEM(2, 128, 1) FI_SMEM(2, 256, 1)
+    FI_SMEM(1, 64, 2) FI_SMEM(1, 128, 2) FI_SMEM(1, 128, 4) FI_SMEM(1, 256, 2) FI_SMEM(1, 256, 4) FI_SMEM(2, 256, 2) FI_SMEM(2, 256, 4) FI_SMEM(2, 128, 2) FI_SMEM(2, 128, 4)
+#undef FI_SMEM
+    return 0;
+}
+
+int tc_gemm_tmem_cols(const TcGemmConfig& c) {
+#define FI_TMEM(CG, BN, SK) \
+    if (c.cta_group == CG && c.bn == BN && c.split_k == SK) return GemmShape<CG, BN, SK>::TMEM_COLS;
+    FI_TMEM(1, 64, 1) FI_TMEM(1, 128, 1) FI_TMEM(1, 256, 1)
+    FI_TMEM(2, 128, 1) FI_TMEM(2, 256, 1)
+    FI_TMEM(1, 64, 2) FI_TMEM(1, 128, 2) FI_TMEM(1, 128, 4) FI_TMEM(1, 256, 2) FI_TMEM(1, 256, 4) FI_TMEM(2, 256, 2) FI_TMEM(2, 256, 4) FI_TMEM(2, 128, 2) FI_TMEM(2, 128, 4)
+#undef FI_TMEM
+    return 0;
+}
+
+int tc_gemm_check(const TcGemmConfig& c, int M, int N, int K) {
+    if (!tc_gemm_stages(c)) return kTcErrUnsupported;
+    const int bm = 128 * c.cta_group;
+    if (M <= 0 || N <= 0 || K <= 0) return kTcErrShape;
+    if (M % bm || N % c.bn || K % (64 * c.split_k)) return kTcErrShape;
+    if (c.b_mn_major && (c.bn / c.cta_group) % 64) return kTcErrShape;
+    if (c.split_k > 1 && (c.bn / c.split_k) % 32) return kTcErrShape;
+    return kTcOk;
+}
+
+int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream) {
+    int chk = tc_gemm_check(cfg, p.M, p.N, p.K);
+    if (chk != kTcOk) return chk;
+#define FI_LAUNCH(CG, BN, SK) \
+    if (cfg.cta_group == CG && cfg.bn == BN && cfg.split_k == SK) return launch_impl<CG, BN, SK>(cfg, p, stream);
+    FI_LAUNCH(1, 64, 1) FI_LAUNCH(1, 128, 1) FI_LAUNCH(1, 256, 1)
+    FI_LAUNCH(2, 128, 1) FI_LAUNCH(2, 256, 1)
+    FI_LAUNCH(1, 64, 2) FI_LAUNCH(1, 128, 2) FI_LAUNCH(1, 128, 4) FI_LAUNCH(1, 256, 2) FI_LAUNCH(1, 256, 4) FI_LAUNCH(2, 256, 2) FI_LAUNCH(2, 256, 4) FI_LAUNCH(2, 128, 2) FI_LAUNCH(2, 128, 4)
+#undef FI_LAUNCH
+    return kTcErrUnsupported;
+}
+
+}  // namespace fireiron::sm100

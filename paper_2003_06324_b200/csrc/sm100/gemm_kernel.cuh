@@ -1,0 +1,392 @@
+// Warp-specialised, persistent tcgen05 GEMM: the sm_100a lowering of the
+// Fireiron tensor-core strategy
+//
+//   tile BMxBN .to block [.pair]           -> persistent CTA (pair) tile loop
+//   [split K/S .splitk]                    -> S CTAs of a cluster share a tile
+//   epilog tm { init {TMEM_ZERO} store {tile 32 BN .to warp; TMEM_STORE} }
+//   split 64 .stages S                     -> S-deep TMA/MMA mbarrier ring
+//   load a sh {TMA_LOAD}  load b sh {TMA_LOAD}
+//   done                                   -> UMMA leaf (tcgen05.mma kind::f16)
+//
+// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (leader CTA),
+// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM -> RF -> GL).
+// Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps
+// the main loop of tile i+1. With kCtaGroup == 2 a CTA pair (cluster of 2)
+// computes a 256xBN tile with tcgen05.mma.cta_group::2: each CTA stages its
+// 128 rows of A and BN/2 rows of B; the accumulator rows stay in each CTA's
+// TMEM. Split-K (kSplitK > 1) gives each CTA (pair) of a cluster a K slice of
+// the same output tile; the partial accumulators are published in shared
+// memory (reusing the drained operand ring) and reduced through DSMEM in a
+// fixed rank order (so results are deterministic) before the fused epilog
+// store. Cluster rank = split_rank * kCtaGroup + pair_rank.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "ptx.cuh"
+
+namespace fireiron::sm100 {
+
+enum class OutType : int { F32 = 0, F16 = 1, BF16 = 2 };
+
+struct GemmArgs {
+    void* C = nullptr;
+    long ldc = 0;               // elements
+    int M = 0, N = 0, K = 0;
+    int tiles_m = 0, tiles_n = 0;
+    int k_blocks = 0;           // 64-wide K blocks per work unit (K / 64 / splits)
+    int ab_format = 0;          // 0 = f16, 1 = bf16 (UMMA a/b format field)
+    int a_mn_major = 0;         // A stored M-contiguous (col-major M x K)
+    int b_mn_major = 0;         // B stored N-contiguous (row-major K x N)
+    int c_row_major = 0;
+    int out_type = 0;           // OutType
+    int group_m = 8;            // raster band (tile rows) for the default order
+    int stages = 0;             // pipeline depth actually used (0 = deepest that fits)
+    const int* tile_order = nullptr;  // optional permutation: Fireiron block-swizzle table
+};
+
+template <int kCtaGroup, int BN, int kSplitK>
+struct GemmShape {
+    static constexpr int BM = 128;                 // rows per CTA (TMEM lanes)
+    static constexpr int BM_TILE = 128 * kCtaGroup;
+    static constexpr int BK = 64;                  // one 128B swizzle span of 16-bit
+    static constexpr int BN_LOCAL = BN / kCtaGroup;
+    static constexpr int A_BYTES = BM * BK * 2;
+    static constexpr int B_BYTES = BN_LOCAL * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    // split-K reduction scratch: the fp32 partial tile (rows padded by 16B)
+    // reuses the operand ring once the tile's main loop has drained it
+    static constexpr int RED_LD = BN + 4;
+    static constexpr int RED_BYTES = kSplitK > 1 ? BM * RED_LD * 4 : 0;
+    static constexpr int kStages = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+    static_assert(kStages >= 2, "pipeline needs at least two stages");
+    static constexpr int kAccBufs = 2;
+    static constexpr int TMEM_COLS_RAW = kAccBufs * BN;
+    static constexpr int TMEM_COLS = TMEM_COLS_RAW <= 32    ? 32
+                                     : TMEM_COLS_RAW <= 64  ? 64
+                                     : TMEM_COLS_RAW <= 128 ? 128
+                                     : TMEM_COLS_RAW <= 256 ? 256
+                                                            : 512;
+    static constexpr int RING_BYTES = kStages * STAGE_BYTES;
+    static constexpr int BAR_BYTES = 256;
+    static_assert(RED_BYTES <= RING_BYTES, "split-K scratch must fit in the operand ring");
+    static constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + 1024;  // + align slack
+    static constexpr int kThreads = 256;
+};
+
+// Tile id -> (tile row, tile col). With an explicit order table (the strategy's
+// Block .swizzle) the unit id maps RowMajor as in Fireiron: row = u % tiles_m.
+// Otherwise a grouped raster keeps a band of group_m A panels L2-resident while
+// sweeping N.
+__device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, int& tn) {
+    if (a.tile_order) {
+        const int u = a.tile_order[t];
+        tm = u % a.tiles_m;
+        tn = u / a.tiles_m;
+        return;
+    }
+    const int band = a.group_m * a.tiles_n;
+    const int g = t / band;
+    const int local = t - g * band;
+    int rows = a.tiles_m - g * a.group_m;
+    if (rows > a.group_m) rows = a.group_m;
+    tm = g * a.group_m + local % rows;
+    tn = local / rows;
+}
+
+template <typename T>
+__device__ __forceinline__ T cvt_out(float v);
+template <>
+__device__ __forceinline__ float cvt_out<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __half cvt_out<__half>(float v) { return __float2half_rn(v); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v) {
+    return __float2bfloat16_rn(v);
+}
+
+// Store 32 consecutive columns of one accumulator row. Column-major C (the
+// Fireiron default) makes each per-column store a coalesced 32-lane segment.
+template <typename T>
+__device__ __forceinline__ void store_row32(const GemmArgs& a, int m, int n, const float (&v)[32]) {
+    T* C = static_cast<T*>(a.C);
+    if (a.c_row_major) {
+        T* p = C + static_cast<long>(m) * a.ldc + n;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) p[j] = cvt_out<T>(v[j]);
+    } else {
+        T* p = C + static_cast<long>(n) * a.ldc + m;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) p[static_cast<long>(j) * a.ldc] = cvt_out<T>(v[j]);
+    }
+}
+
+__device__ __forceinline__ void store_row32_any(const GemmArgs& a, int m, int n,
+                                                const float (&v)[32]) {
+    switch (static_cast<OutType>(a.out_type)) {
+        case OutType::F32: store_row32<float>(a, m, n, v); break;
+        case OutType::F16: store_row32<__half>(a, m, n, v); break;
+        case OutType::BF16: store_row32<__nv_bfloat16>(a, m, n, v); break;
+    }
+}
+
+// Kernel body; the tensor maps must be __grid_constant__ kernel parameters
+// (TMA reads them through their parameter-space address).
+template <int kCtaGroup, int BN, int kSplitK>
+__device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
+                                                   const GemmArgs& args) {
+    using S = GemmShape<kCtaGroup, BN, kSplitK>;
+    constexpr int kStages = S::kStages;
+    constexpr int kClusterSize = kCtaGroup * kSplitK;
+
+    extern __shared__ uint8_t smem_raw[];
+    // 1024B alignment for the 128B-swizzle atoms
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+    uint8_t* ring = smem;
+    float* red = reinterpret_cast<float*>(ring);  // split-K scratch (ring reuse)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::RING_BYTES);
+    uint64_t* full_bar = bars;                      // [kStages] TMA -> MMA
+    uint64_t* empty_bar = bars + kStages;           // [kStages] MMA -> TMA
+    uint64_t* tfull_bar = bars + 2 * kStages;       // [2] MMA -> epilogue
+    uint64_t* tempty_bar = bars + 2 * kStages + 2;  // [2] epilogue -> MMA
+    uint64_t* rfull_bar = bars + 2 * kStages + 4;   // split-K: all partials published
+    uint64_t* rempty_bar = bars + 2 * kStages + 5;  // split-K: all peers done reading
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t crank = kClusterSize > 1 ? cluster_ctarank() : 0;
+    const uint32_t pair_rank = crank % kCtaGroup;   // position inside the CTA pair
+    const uint32_t split_rank = crank / kCtaGroup;  // K slice owned by this CTA
+    const bool mma_leader = pair_rank == 0;
+    const uint16_t pair_mask = static_cast<uint16_t>(3u << (crank - pair_rank));
+
+    if (threadIdx.x == 32) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull_bar[b], 1);
+            mbar_init(&tempty_bar[b], 4 * kCtaGroup);
+        }
+        mbar_init(rfull_bar, 4 * kSplitK);
+        mbar_init(rempty_bar, 4 * kSplitK);
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 2) tmem_alloc<kCtaGroup>(tmem_slot, S::TMEM_COLS);
+    tc_fence_before();
+    if constexpr (kClusterSize > 1) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int nst = (args.stages > 0 && args.stages < kStages) ? args.stages : kStages;
+    const int num_tiles = args.tiles_m * args.tiles_n;
+    const int cluster = blockIdx.x / kClusterSize;
+    const int nclusters = gridDim.x / kClusterSize;
+    const int kb0 = static_cast<int>(split_rank) * args.k_blocks;  // first K block of my slice
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int t = cluster; t < num_tiles; t += nclusters, ++it) {
+                int tm, tn;
+                tile_coords(args, t, tm, tn);
+                if constexpr (kSplitK > 1) {
+                    // the ring doubles as the reduction scratch: wait until every
+                    // peer has read my previous partial tile
+                    mbar_wait_cluster(rempty_bar, (static_cast<uint32_t>(it) & 1) ^ 1);
+                    fence_proxy_async();
+                }
+                const int m0 = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
+                const int n0 = tn * BN + static_cast<int>(pair_rank) * S::BN_LOCAL;
+                for (int kb = 0; kb < args.k_blocks; ++kb) {
+                    mbar_wait(&empty_bar[s], ph ^ 1);
+                    uint8_t* sa = ring + s * S::STAGE_BYTES;
+                    uint8_t* sb = sa + S::A_BYTES;
+                    const int k0 = (kb0 + kb) * S::BK;
+                    if (mma_leader) mbar_arrive_expect_tx(&full_bar[s], S::STAGE_BYTES * kCtaGroup);
+                    auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
+                        if constexpr (kCtaGroup == 1) tma_load_2d(dst, map, &full_bar[s], c0, c1);
+                        else tma_load_2d_pair(dst, map, &full_bar[s], c0, c1);
+                    };
+                    if (args.a_mn_major) {
+                        load(sa, &tmA, m0, k0);
+                        load(sa + 8192, &tmA, m0 + 64, k0);
+                    } else {
+                        load(sa, &tmA, k0, m0);
+                    }
+                    if (args.b_mn_major) {
+#pragma unroll
+                        for (int j = 0; j < S::BN_LOCAL / 64; ++j)
+                            load(sb + j * 8192, &tmB, n0 + j * 64, k0);
+                    } else {
+                        load(sb, &tmB, k0, n0);
+                    }
+                    if (++s == nst) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (mma_leader && lane == 0) {
+            // instruction descriptor: f32 accumulate, a/b format, majors, N>>3, M>>4
+            const uint32_t idesc = (1u << 4) | (static_cast<uint32_t>(args.ab_format) << 7) |
+                                   (static_cast<uint32_t>(args.ab_format) << 10) |
+                                   (static_cast<uint32_t>(args.a_mn_major) << 15) |
+                                   (static_cast<uint32_t>(args.b_mn_major) << 16) |
+                                   (static_cast<uint32_t>(BN >> 3) << 17) |
+                                   (static_cast<uint32_t>(S::BM_TILE >> 4) << 24);
+            // K-major: rows of 128B, 8-row atoms 1024B apart (SBO), K step = 32B.
+            // MN-major: 64-element chunks 8KB apart (LBO), 8 k-rows per atom (SBO 1KB),
+            //           K step of 16 = two atoms = 2KB.
+            const uint32_t a_lbo = args.a_mn_major ? 8192 : 16, a_kstep = args.a_mn_major ? 2048 : 32;
+            const uint32_t b_lbo = args.b_mn_major ? 8192 : 16, b_kstep = args.b_mn_major ? 2048 : 32;
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int t = cluster; t < num_tiles; t += nclusters, ++it) {
+                const int buf = it & 1;
+                const uint32_t use = static_cast<uint32_t>(it >> 1);
+                mbar_wait_cluster(&tempty_bar[buf], (use & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+                for (int kb = 0; kb < args.k_blocks; ++kb) {
+                    mbar_wait(&full_bar[s], ph);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(ring + s * S::STAGE_BYTES);
+                    const uint32_t sb = sa + S::A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < S::BK / 16; ++k) {
+                        uint64_t ad = smem_desc_sw128(sa + k * a_kstep, a_lbo, 1024);
+                        uint64_t bd = smem_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
+                        umma_f16<kCtaGroup>(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    if constexpr (kCtaGroup == 1) umma_commit(&empty_bar[s]);
+                    else umma_commit_pair(&empty_bar[s], pair_mask);
+                    if (++s == nst) { s = 0; ph ^= 1; }
+                }
+                if constexpr (kCtaGroup == 1) umma_commit(&tfull_bar[buf]);
+                else umma_commit_pair(&tfull_bar[buf], pair_mask);
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp - 4;  // TMEM lane quarter owned by this warp
+        const int row = q * 32 + lane;
+        int it = 0;
+        for (int t = cluster; t < num_tiles; t += nclusters, ++it) {
+            int tm, tn;
+            tile_coords(args, t, tm, tn);
+            const int buf = it & 1;
+            const uint32_t use = static_cast<uint32_t>(it >> 1);
+            mbar_wait(&tfull_bar[buf], use & 1);
+            tc_fence_after();
+            const int m = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM + row;
+            const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                   static_cast<uint32_t>(buf * BN);
+            if constexpr (kSplitK == 1) {
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tbase + c * 32, r);
+                    tmem_ld_wait();
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                    store_row32_any(args, m, tn * BN + c * 32, v);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (kCtaGroup == 1) mbar_arrive(&tempty_bar[buf]);
+                    else mbar_arrive_cluster(&tempty_bar[buf], crank - pair_rank);
+                }
+            } else {
+                const uint32_t tile_use = static_cast<uint32_t>(it);
+                // The producer only refills the ring after rempty completes, and
+                // tfull implies this tile's operands are consumed: the ring is free.
+                float* my_row = red + row * S::RED_LD;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tbase + c * 32, r);
+                    tmem_ld_wait();
+                    float4* dst = reinterpret_cast<float4*>(my_row + c * 32);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                             __uint_as_float(r[4 * j + 2]),
+                                             __uint_as_float(r[4 * j + 3]));
+                }
+                tc_fence_before();
+                fence_acq_rel_cluster();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (kCtaGroup == 1) mbar_arrive(&tempty_bar[buf]);
+                    else mbar_arrive_cluster(&tempty_bar[buf], crank - pair_rank);
+#pragma unroll 1
+                    for (int r = 0; r < kSplitK; ++r)
+                        mbar_arrive_cluster(rfull_bar, static_cast<uint32_t>(r * kCtaGroup) + pair_rank);
+                }
+                mbar_wait_cluster(rfull_bar, tile_use & 1);
+                // reduce the column slice owned by this split rank, rank order 0..S-1
+                constexpr int kCols = BN / kSplitK;
+                const int c0 = static_cast<int>(split_rank) * kCols;
+                const uint32_t my_addr = smem_u32(my_row + c0);
+#pragma unroll 1
+                for (int cc = 0; cc < kCols; cc += 32) {
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+#pragma unroll 1
+                    for (int r = 0; r < kSplitK; ++r) {
+                        const uint32_t peer = static_cast<uint32_t>(r * kCtaGroup) + pair_rank;
+                        const uint32_t base = map_shared_rank(my_addr + cc * 4, peer);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            float4 x = ld_dsmem_f4(base + j * 16);
+                            v[4 * j + 0] += x.x;
+                            v[4 * j + 1] += x.y;
+                            v[4 * j + 2] += x.z;
+                            v[4 * j + 3] += x.w;
+                        }
+                    }
+                    store_row32_any(args, m, tn * BN + c0 + cc, v);
+                }
+                fence_proxy_async();
+                fence_acq_rel_cluster();
+                __syncwarp();
+                if (lane == 0)
+                    for (int r = 0; r < kSplitK; ++r)
+                        mbar_arrive_cluster(rempty_bar, static_cast<uint32_t>(r * kCtaGroup) + pair_rank);
+            }
+        }
+    }
+
+    tc_fence_before();
+    if constexpr (kClusterSize > 1) cluster_sync(); else __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<kCtaGroup>(tmem_base, S::TMEM_COLS);
+    }
+}
+
+template <int kCtaGroup, int BN, int kSplitK>
+__global__ void __launch_bounds__(256, 1)
+    fi_sm100_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const __grid_constant__ GemmArgs args) {
+    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK>(tmA, tmB, args);
+}
+
+}  // namespace fireiron::sm100

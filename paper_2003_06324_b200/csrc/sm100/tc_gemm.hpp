@@ -1,0 +1,45 @@
+// Host interface of the sm_100a tensor-core GEMM family (no CUDA headers needed
+// beyond cudaStream_t).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace fireiron::sm100 {
+
+constexpr int kTcOk = 0;
+constexpr int kTcErrShape = 1;
+constexpr int kTcErrUnsupported = 2;
+constexpr int kTcErrTensorMap = 3;
+constexpr int kTcErrCuda = 4;
+
+struct TcGemmConfig {
+    int cta_group = 2;   // 1: tcgen05 cta_group::1, M tile 128; 2: CTA pair, M tile 256
+    int bn = 256;        // N tile (UMMA N)
+    int split_k = 1;     // CTAs of a cluster sharing one output tile (K slices)
+    int ab_format = 0;   // 0 = f16, 1 = bf16
+    int a_mn_major = 1;  // A col-major (Fireiron default)
+    int b_mn_major = 0;  // B col-major => K-major (Fireiron default)
+    int c_row_major = 0;
+    int out_type = 0;    // 0 f32, 1 f16, 2 bf16
+    int group_m = 8;     // raster band for the default tile order
+    int stages = 0;      // pipeline depth (0 = deepest that fits in shared memory)
+};
+
+struct TcGemmProblem {
+    const void* A = nullptr;
+    const void* B = nullptr;
+    void* C = nullptr;
+    int M = 0, N = 0, K = 0;
+    long lda = 0, ldb = 0, ldc = 0;  // elements, physical leading dimension
+    const int* tile_order = nullptr; // device array, tiles_m*tiles_n entries, or null
+    int num_sms = 148;
+    int max_ctas = 0;                // 0 = persistent over all SMs
+};
+
+int tc_gemm_check(const TcGemmConfig& c, int M, int N, int K);
+int tc_gemm_stages(const TcGemmConfig& c);
+int tc_gemm_smem_bytes(const TcGemmConfig& c);
+int tc_gemm_tmem_cols(const TcGemmConfig& c);
+int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream);
+
+}  // namespace fireiron::sm100

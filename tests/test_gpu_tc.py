@@ -1,0 +1,124 @@
+"""GPU parity of the tensor-core (tcgen05/TMA/TMEM) strategies. Integer-mode
+inputs ({-3..3}, exact in f16/bf16, partial sums < 2^24) must equal the fp64
+oracle exactly for every strategy, split-K included; uniform inputs must meet
+the north-star bound max|C - C64| / max|C64| <= 1e-2 with C64 the fp64 GEMM
+on grid-rounded inputs (tolerance stated here: 1e-2)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_NORMWISE = 1e-2
+
+
+def run(fi, oracle, script, m, n, k, integers, seed=1, elem="f16"):
+    plan = fi.Plan(script)
+    assert plan.kind == "tcgen05", plan.source()[:200]
+    a = oracle.fill(m, k, seed, integers)
+    b = oracle.fill(k, n, seed + 1, integers)
+    c = plan.run_host(a, b)
+    ar, br = oracle.round_elem(a, elem), oracle.round_elem(b, elem)
+    return c, ar, br
+
+
+CFGS = [dict(pair=True, tile_n=256), dict(pair=True, tile_n=128), dict(pair=False, tile_n=256),
+        dict(pair=False, tile_n=128), dict(pair=False, tile_n=64)]
+LAYOUTS = [("colmajor", "colmajor", "colmajor"), ("rowmajor", "colmajor", "colmajor"),
+           ("colmajor", "rowmajor", "rowmajor"), ("rowmajor", "rowmajor", "colmajor")]
+
+
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: f"pair{int(c['pair'])}_n{c['tile_n']}")
+@pytest.mark.parametrize("layouts", LAYOUTS, ids=lambda l: "".join(x[0] for x in l))
+def test_integer_exact_all_tiles_and_layouts(fi, oracle, cfg, layouts):
+    m, n, k = 512, 768 if cfg["tile_n"] != 256 else 512, 320
+    s = fi.strategies.tc_strategy(m, n, k, layouts=layouts, **cfg)
+    c, ar, br = run(fi, oracle, s, m, n, k, True)
+    assert np.array_equal(c, oracle.gemm_f64(ar, br))
+
+
+@pytest.mark.parametrize("ab", ["f16", "bf16"])
+@pytest.mark.parametrize("cout", ["f32", "f16", "bf16"])
+def test_element_types(fi, oracle, ab, cout):
+    m, n, k = 512, 512, 256
+    s = fi.strategies.tc_strategy(m, n, k, ab=ab, c=cout)
+    c, ar, br = run(fi, oracle, s, m, n, k, False, elem=ab)
+    want = oracle.gemm_f64(ar, br)
+    err = np.max(np.abs(c - want)) / np.max(np.abs(want))
+    bound = TOL_NORMWISE if cout == "f32" else 2.0 ** -7
+    assert err <= bound
+    if cout == "f32":
+        assert err <= 1e-5  # fp32 accumulation on exact products
+
+
+@pytest.mark.parametrize("pair,tile_n,split", [(False, 128, 2), (False, 128, 4), (False, 256, 4),
+                                               (True, 256, 2), (True, 256, 4), (True, 128, 2)])
+def test_splitk_integer_exact_and_deterministic(fi, oracle, pair, tile_n, split):
+    m, n, k = 512, 512, 4096
+    s = fi.strategies.tc_strategy(m, n, k, pair=pair, tile_n=tile_n, split_k=split)
+    c, ar, br = run(fi, oracle, s, m, n, k, True)
+    assert np.array_equal(c, oracle.gemm_f64(ar, br))
+    plan = fi.Plan(s)
+    a = oracle.fill(m, k, 9, False)
+    b = oracle.fill(k, n, 10, False)
+    c1, c2 = plan.run_host(a, b), plan.run_host(a, b)
+    assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))  # fixed reduction order
+
+
+def test_c2_strategy_4096_uniform_within_tolerance(fi, oracle):
+    s = fi.strategies.c2_strategy()
+    c, ar, br = run(fi, oracle, s, 4096, 4096, 4096, False, seed=1)
+    rng = np.random.default_rng(0)
+    rows = rng.integers(0, 4096, 4096)
+    cols = rng.integers(0, 4096, 4096)
+    want = oracle.sample_f64(ar, br, rows, cols)
+    got = c[rows, cols].astype(np.float64)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= TOL_NORMWISE
+    assert np.max(np.abs(got - want)) <= 1e-3
+
+
+def test_c2_strategy_4096_integer_exact_sampled(fi, oracle):
+    s = fi.strategies.c2_strategy()
+    c, ar, br = run(fi, oracle, s, 4096, 4096, 4096, True, seed=3)
+    assert np.array_equal(c, np.round(c))
+    rng = np.random.default_rng(1)
+    rows, cols = rng.integers(0, 4096, 8192), rng.integers(0, 4096, 8192)
+    assert np.array_equal(c[rows, cols].astype(np.float64), oracle.sample_f64(ar, br, rows, cols))
+
+
+def test_c3_splitk_strategy_integer_exact_sampled(fi, oracle):
+    s = fi.strategies.c3_strategy()
+    c, ar, br = run(fi, oracle, s, 1024, 1024, 32768, True, seed=5)
+    rng = np.random.default_rng(2)
+    rows, cols = rng.integers(0, 1024, 4096), rng.integers(0, 1024, 4096)
+    assert np.array_equal(c[rows, cols].astype(np.float64), oracle.sample_f64(ar, br, rows, cols))
+
+
+def test_block_swizzle_schedule_is_honoured(fi, oracle):
+    # tiles visited in reverse order: results must not depend on the schedule
+    m, n, k = 1024, 1024, 256
+    units = (m // 256) * (n // 256)
+    s = fi.strategies.tc_strategy(m, n, k, swizzle=f"(id*5)%{units}")  # 5 is coprime with 16
+    c, ar, br = run(fi, oracle, s, m, n, k, True)
+    assert np.array_equal(c, oracle.gemm_f64(ar, br))
+
+
+def test_device_launch_equals_host_run(fi, oracle):
+    import torch
+    m, n, k = 512, 512, 512
+    plan = fi.Plan(fi.strategies.tc_strategy(m, n, k))
+    a = oracle.fill(m, k, 7, False)
+    b = oracle.fill(k, n, 8, False)
+    host = plan.run_host(a, b)
+    da = torch.from_numpy(a.T.copy()).cuda().half()  # col-major A
+    db = torch.from_numpy(b.T.copy()).cuda().half()  # col-major B
+    dc = torch.empty((n, m), device="cuda")
+    plan.launch(da.data_ptr(), db.data_ptr(), dc.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(dc.cpu().numpy().T.view(np.uint32), host.view(np.uint32))
+
+
+def test_unsupported_tile_reports_cleanly(fi):
+    s = fi.strategies.tc_strategy(512, 480, 256, pair=False, tile_n=96)
+    with pytest.raises(fi.FiError) as e:
+        fi.Plan(s)
+    assert e.value.kind in ("Unsupported", "NonDivisible")
