@@ -95,6 +95,7 @@ struct PlanInfo {
     long grid_x = 1, grid_y = 1, block_threads = 1;
     long launch_ctas = 0;
     int cluster = 1, stages = 0, tmem_cols = 0, cta_group = 1, tile_m = 0, tile_n = 0, split_k = 1;
+    int streamk = 0;  // tcgen05 plans: stream-K work partitioning in use
     long shared_bytes = 0;
     double flops = 0.0;
     std::string entry_name;
@@ -113,6 +114,10 @@ public:
     void launch(const void* dA, const void* dB, void* dC, void* stream) const;
     // anvil::run semantics on host fp32 matrices (grid snapping on ingestion)
     RunResult run_host(const Matrix& a, const Matrix* b, void* stream = nullptr) const;
+    // Same on raw host fp32 arrays in the root physical layouts (extent
+    // elements each; pinned memory makes the copies asynchronous DMA).
+    // Returns the kernel time in ms.
+    double run_host_raw(const float* A, const float* B, float* C, void* stream = nullptr) const;
 
     const PlanInfo& info() const;
     const Program& program() const;

@@ -66,6 +66,8 @@ typedef struct fi_plan_info {
     int32_t cta_group, tile_m, tile_n, split_k;
     int64_t shared_bytes;         /* dynamic smem per CTA                       */
     double flops;                 /* 2*M*N*K (0 for Move)                       */
+    int32_t streamk;              /* stream-K partitioning of (tile, K-block) work */
+    int32_t reserved;
     char entry_name[128];
 } fi_plan_info;
 
@@ -76,6 +78,8 @@ fi_status fi_plan_create(const char* script_utf8, int64_t m, int64_t n, int64_t 
                          uint32_t flags, fi_plan* out);
 
 /* Asynchronous, stream-ordered execution on device buffers the caller owns.
+ * Launches of one plan must be ordered on one stream (tensor-core plans keep
+ * a stream-K partial workspace per plan); use one plan per concurrent stream.
  * Buffers hold the root spec's element types in the root layouts. For Move
  * roots dB is ignored and dA/dC are src/dst. C is fully overwritten (the
  * reference zero-initialises the root C, sim.hpp:222-223). */

@@ -57,7 +57,8 @@ class PlanInfo(C.Structure):
                 ("block_threads", C.c_int64), ("launch_ctas", C.c_int64), ("cluster", C.c_int32),
                 ("stages", C.c_int32), ("tmem_cols", C.c_int32), ("cta_group", C.c_int32),
                 ("tile_m", C.c_int32), ("tile_n", C.c_int32), ("split_k", C.c_int32),
-                ("shared_bytes", C.c_int64), ("flops", C.c_double), ("entry_name", C.c_char * 128)]
+                ("shared_bytes", C.c_int64), ("flops", C.c_double), ("streamk", C.c_int32),
+                ("reserved", C.c_int32), ("entry_name", C.c_char * 128)]
 
 
 def _load() -> C.CDLL:

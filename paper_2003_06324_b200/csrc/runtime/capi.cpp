@@ -82,26 +82,9 @@ fi_status fi_plan_launch(fi_plan plan, const void* dA, const void* dB, void* dC,
 fi_status fi_plan_run_host(fi_plan plan, const float* A, const float* B, float* C) {
     if (!plan || !A || !C) return rt::set_error(FI_ERR_ARGUMENT, "fi_plan_run_host: null argument");
     return guarded([&] {
-        const Program& prog = plan->plan->program();
-        const BufferDecl& ra = prog.plan.at(0);
-        Matrix a;
-        a.rows = ra.rows;
-        a.cols = ra.cols;
-        a.layout = ra.layout;
-        a.data.assign(A, A + ra.extent());
-        Matrix b;
-        const Matrix* bp = nullptr;
-        if (prog.root.is_matmul()) {
-            if (!B) return rt::set_error(FI_ERR_ARGUMENT, "fi_plan_run_host: matmul needs B");
-            const BufferDecl& rb = prog.plan.at(1);
-            b.rows = rb.rows;
-            b.cols = rb.cols;
-            b.layout = rb.layout;
-            b.data.assign(B, B + rb.extent());
-            bp = &b;
-        }
-        RunResult r = plan->plan->run_host(a, bp, nullptr);
-        std::memcpy(C, r.output.data.data(), r.output.data.size() * sizeof(float));
+        if (plan->plan->program().root.is_matmul() && !B)
+            return rt::set_error(FI_ERR_ARGUMENT, "fi_plan_run_host: matmul needs B");
+        plan->plan->run_host_raw(A, B, C, nullptr);
         return FI_OK;
     });
 }
@@ -143,6 +126,7 @@ fi_status fi_plan_query(fi_plan plan, fi_plan_info* info) {
         info->split_k = pi.split_k;
         info->shared_bytes = pi.shared_bytes;
         info->flops = pi.flops;
+        info->streamk = pi.streamk;
         std::strncpy(info->entry_name, pi.entry_name.c_str(), sizeof(info->entry_name) - 1);
         return FI_OK;
     });

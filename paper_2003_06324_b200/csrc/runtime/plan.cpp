@@ -244,11 +244,13 @@ struct Plan::Impl {
     sm100::TcGemmConfig tc;
     sm100::TcGemmProblem tp;
     int32_t* d_tile_order = nullptr;
+    mutable sm100::TcWorkspace ws;  // stream-K partials + epoch flags of this plan
     // run_host scratch
     mutable std::mutex mu;
     mutable void* scratch = nullptr;
     mutable size_t scratch_bytes = 0;
     mutable cudaStream_t own_stream = nullptr;
+    mutable cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     ~Impl() {
         if (module) {
@@ -260,6 +262,8 @@ struct Plan::Impl {
         if (d_tile_order) cudaFree(d_tile_order);
         if (scratch) cudaFree(scratch);
         if (own_stream) cudaStreamDestroy(own_stream);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
     }
 
     const BufferDecl& root(int i) const { return prog.plan.at(i); }
@@ -341,9 +345,10 @@ std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const 
         info.stages = sm100::tc_gemm_stages(c);
         info.tmem_cols = sm100::tc_gemm_tmem_cols(c);
         info.shared_bytes = sm100::tc_gemm_smem_bytes(c);
-        const long tiles = (root.m() / tc.tile_m) * (root.n() / tc.tile_n);
-        const long clusters = std::min<long>(tiles, p.num_sms / info.cluster);
-        info.launch_ctas = clusters * info.cluster;
+        if (const char* e = std::getenv("FI_STREAMK")) p.streamk = std::atoi(e);
+        const sm100::TcLaunchInfo li = sm100::tc_gemm_plan(c, p);
+        info.launch_ctas = li.ctas;
+        info.streamk = li.streamk;
         impl->source = generate(prog).source;
         return std::shared_ptr<Plan>(new Plan(std::move(impl)));
     }
@@ -371,6 +376,7 @@ void Plan::launch(const void* dA, const void* dB, void* dC, void* stream) const 
     auto s = static_cast<cudaStream_t>(stream);
     if (I.info.kind == 1) {
         sm100::TcGemmProblem p = I.tp;
+        p.workspace = &I.ws;
         p.A = dA;
         p.B = dB;
         p.C = dC;
@@ -406,7 +412,7 @@ void Plan::launch(const void* dA, const void* dB, void* dC, void* stream) const 
               "cuLaunchKernel");
 }
 
-RunResult Plan::run_host(const Matrix& a, const Matrix* b, void* stream) const {
+double Plan::run_host_raw(const float* A, const float* B, float* C, void* stream) const {
     const Impl& I = *impl_;
     const Spec& root = I.prog.root;
     std::lock_guard<std::mutex> g(I.mu);
@@ -417,19 +423,12 @@ RunResult Plan::run_host(const Matrix& a, const Matrix* b, void* stream) const {
         s = I.own_stream;
     }
     const int nin = root.is_matmul() ? 2 : 1;
-    const Matrix* ins[2] = {&a, b};
-    if (root.is_matmul() && !b) fail(ErrorKind::ShapeMismatch, "matmul execution needs both A and B inputs");
-    for (int i = 0; i < nin; ++i) {
-        const BufferDecl& r = I.root(i);
-        if (ins[i]->rows != r.rows || ins[i]->cols != r.cols)
-            fail(ErrorKind::ShapeMismatch, "input for " + r.name + " must be " + std::to_string(r.rows) + "x" +
-                                               std::to_string(r.cols));
-    }
+    const float* ins[2] = {A, B};
+    if (root.is_matmul() && !B) fail(ErrorKind::ShapeMismatch, "matmul execution needs both A and B inputs");
     const BufferDecl& out = I.root(I.out_root());
-    // scratch layout: [f32 staging of each input][typed inputs][typed C][f32 C]
+    // scratch: [f32 staging of each input][typed inputs][typed C][f32 C]
     auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
-    size_t off = 0;
-    size_t f32_in[2] = {0, 0}, typed_in[2] = {0, 0};
+    size_t off = 0, f32_in[2] = {0, 0}, typed_in[2] = {0, 0};
     for (int i = 0; i < nin; ++i) {
         f32_in[i] = off;
         off = align(off + static_cast<size_t>(I.root(i).extent()) * 4);
@@ -450,43 +449,70 @@ RunResult Plan::run_host(const Matrix& a, const Matrix* b, void* stream) const {
     }
     auto* base = static_cast<char*>(I.scratch);
     for (int i = 0; i < nin; ++i) {
-        // the host Matrix stores the root's physical layout; pads carry zeros
         const BufferDecl& r = I.root(i);
-        if (static_cast<long>(ins[i]->data.size()) != r.extent() || !(ins[i]->layout == r.layout)) {
-            Matrix tmp = Matrix::zeros(r.rows, r.cols, r.layout);
-            for (long rr = 0; rr < r.rows; ++rr)
-                for (long cc = 0; cc < r.cols; ++cc) tmp.at(rr, cc) = ins[i]->at(rr, cc);
-            ck(cudaMemcpyAsync(base + f32_in[i], tmp.data.data(), tmp.data.size() * 4, cudaMemcpyHostToDevice, s),
-               "cudaMemcpyAsync");
-            ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-        } else {
-            ck(cudaMemcpyAsync(base + f32_in[i], ins[i]->data.data(), ins[i]->data.size() * 4,
+        if (r.elem == ElemType::F32) {  // copy straight into the typed buffer
+            ck(cudaMemcpyAsync(base + typed_in[i], ins[i], static_cast<size_t>(r.extent()) * 4,
                                cudaMemcpyHostToDevice, s),
                "cudaMemcpyAsync");
+            continue;
         }
+        ck(cudaMemcpyAsync(base + f32_in[i], ins[i], static_cast<size_t>(r.extent()) * 4, cudaMemcpyHostToDevice, s),
+           "cudaMemcpyAsync");
+        // snapping to the root's element grid on ingestion (sim.hpp:507-510)
         ck(rt::convert_f32(reinterpret_cast<float*>(base + f32_in[i]), base + typed_in[i], r.extent(),
                            elem_code(r.elem), s),
            "input conversion");
     }
-    cudaEvent_t e0, e1;
-    ck(cudaEventCreate(&e0), "cudaEventCreate");
-    ck(cudaEventCreate(&e1), "cudaEventCreate");
-    ck(cudaEventRecord(e0, s), "cudaEventRecord");
+    if (!I.ev0) {
+        ck(cudaEventCreate(&I.ev0), "cudaEventCreate");
+        ck(cudaEventCreate(&I.ev1), "cudaEventCreate");
+    }
+    ck(cudaEventRecord(I.ev0, s), "cudaEventRecord");
     launch(base + typed_in[0], nin > 1 ? base + typed_in[1] : nullptr, base + typed_c, s);
-    ck(cudaEventRecord(e1, s), "cudaEventRecord");
-    ck(rt::widen_to_f32(base + typed_c, reinterpret_cast<float*>(base + f32_c), out.extent(), elem_code(out.elem), s),
-       "output conversion");
-    RunResult res;
-    res.output = Matrix::zeros(out.rows, out.cols, out.layout);
-    ck(cudaMemcpyAsync(res.output.data.data(), base + f32_c, static_cast<size_t>(out.extent()) * 4,
-                       cudaMemcpyDeviceToHost, s),
+    ck(cudaEventRecord(I.ev1, s), "cudaEventRecord");
+    const void* result = base + typed_c;
+    if (out.elem != ElemType::F32) {
+        ck(rt::widen_to_f32(base + typed_c, reinterpret_cast<float*>(base + f32_c), out.extent(),
+                            elem_code(out.elem), s),
+           "output conversion");
+        result = base + f32_c;
+    }
+    ck(cudaMemcpyAsync(C, result, static_cast<size_t>(out.extent()) * 4, cudaMemcpyDeviceToHost, s),
        "cudaMemcpyAsync");
     ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    res.device_ms = ms;
+    cudaEventElapsedTime(&ms, I.ev0, I.ev1);
+    return ms;
+}
+
+RunResult Plan::run_host(const Matrix& a, const Matrix* b, void* stream) const {
+    const Impl& I = *impl_;
+    const Spec& root = I.prog.root;
+    const int nin = root.is_matmul() ? 2 : 1;
+    const Matrix* ins[2] = {&a, b};
+    if (root.is_matmul() && !b) fail(ErrorKind::ShapeMismatch, "matmul execution needs both A and B inputs");
+    std::vector<float> staged[2];
+    const float* ptr[2] = {nullptr, nullptr};
+    for (int i = 0; i < nin; ++i) {
+        const BufferDecl& r = I.root(i);
+        if (ins[i]->rows != r.rows || ins[i]->cols != r.cols)
+            fail(ErrorKind::ShapeMismatch, "input for " + r.name + " must be " + std::to_string(r.rows) + "x" +
+                                               std::to_string(r.cols));
+        if (static_cast<long>(ins[i]->data.size()) == r.extent() && ins[i]->layout == r.layout) {
+            ptr[i] = ins[i]->data.data();
+            continue;
+        }
+        // re-lay the logical matrix into the root's physical layout (pads = 0)
+        Matrix tmp = Matrix::zeros(r.rows, r.cols, r.layout);
+        for (long rr = 0; rr < r.rows; ++rr)
+            for (long cc = 0; cc < r.cols; ++cc) tmp.at(rr, cc) = ins[i]->at(rr, cc);
+        staged[i] = std::move(tmp.data);
+        ptr[i] = staged[i].data();
+    }
+    const BufferDecl& out = I.root(I.out_root());
+    RunResult res;
+    res.output = Matrix::zeros(out.rows, out.cols, out.layout);
+    res.device_ms = run_host_raw(ptr[0], ptr[1], res.output.data.data(), stream);
     return res;
 }
 

@@ -47,8 +47,15 @@ CUresult encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, u
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
+thread_local TcLaunchInfo g_last;
+
+TcWorkspace* shared_workspace() {
+    static TcWorkspace ws;  // library pool for callers without their own workspace
+    return &ws;
+}
+
 template <int kCtaGroup, int BN, int kSplitK>
-int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream) {
+int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream, bool dry_run = false) {
     using S = GemmShape<kCtaGroup, BN, kSplitK>;
     auto kernel = fi_sm100_gemm<kCtaGroup, BN, kSplitK>;
     constexpr int kCluster = kCtaGroup * kSplitK;
@@ -100,8 +107,6 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     int sms = p.num_sms > 0 ? p.num_sms : 148;
     int clusters = sms / kCluster;
     if (p.max_ctas > 0 && p.max_ctas / kCluster < clusters) clusters = p.max_ctas / kCluster;
-    if (clusters > tiles) clusters = tiles;
-    if (clusters < 1) clusters = 1;
 
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(clusters * kCluster, 1, 1);
@@ -119,11 +124,76 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     }
     lc.attrs = attrs;
     lc.numAttrs = nattr;
+
+    // Stream-K needs every cluster co-resident (owners spin on later
+    // segments' flags): cap the grid at the occupancy limit.
+    static int max_active = -1;
+    if (max_active < 0) {
+        lc.gridDim = dim3(clusters * kCluster, 1, 1);
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kernel, &lc) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = clusters;
+        }
+        max_active = n;
+    }
+    if (clusters > max_active) clusters = max_active;
+    // data-parallel when whole tiles fill the waves well, stream-K otherwise
+    const int kb = args.k_blocks;
+    int sk_clusters = clusters;
+    const long long sk_cap = static_cast<long long>(tiles) * (kb / 8 > 1 ? kb / 8 : 1);
+    if (sk_cap < sk_clusters) sk_clusters = static_cast<int>(sk_cap);
+    const int dp_clusters = clusters < tiles ? clusters : tiles;
+    const int waves = (tiles + dp_clusters - 1) / dp_clusters;
+    const double dp_eff = static_cast<double>(tiles) / (static_cast<double>(waves) * clusters);
+    bool sk = kSplitK == 1 && sk_clusters > 1 &&
+              (p.streamk == 1 || (p.streamk < 0 && dp_eff < 0.95 && tiles % sk_clusters != 0));
+    if (dry_run) {
+        const int c = sk ? sk_clusters : dp_clusters;
+        g_last = TcLaunchInfo{c * kCluster, c, sk ? 1 : 0};
+        return kTcOk;
+    }
+    if (sk) {
+        clusters = sk_clusters;
+        TcWorkspace* ws = p.workspace ? p.workspace : shared_workspace();
+        const size_t need_p = static_cast<size_t>(clusters) * kCtaGroup * S::WS_FLOATS;
+        const size_t need_f = static_cast<size_t>(clusters) * kCtaGroup;
+        if (ws->partial_floats < need_p) {
+            if (ws->partials) cudaFree(ws->partials);
+            ws->partials = nullptr;
+            if (cudaMalloc(&ws->partials, need_p * sizeof(float)) != cudaSuccess) return kTcErrCuda;
+            ws->partial_floats = need_p;
+        }
+        if (ws->flag_count < need_f) {
+            if (ws->flags) cudaFree(ws->flags);
+            ws->flags = nullptr;
+            if (cudaMalloc(&ws->flags, need_f * sizeof(unsigned)) != cudaSuccess) return kTcErrCuda;
+            if (cudaMemsetAsync(ws->flags, 0, need_f * sizeof(unsigned), stream) != cudaSuccess) return kTcErrCuda;
+            ws->flag_count = need_f;
+            ws->epoch = 0;
+        }
+        args.streamk = 1;
+        args.workspace = ws->partials;
+        args.flags = ws->flags;
+        args.epoch = ++ws->epoch;
+    } else {
+        clusters = dp_clusters;
+    }
+    if (clusters < 1) clusters = 1;
+    lc.gridDim = dim3(clusters * kCluster, 1, 1);
+    g_last = TcLaunchInfo{clusters * kCluster, clusters, sk ? 1 : 0};
     cudaError_t e = cudaLaunchKernelEx(&lc, kernel, tmA, tmB, args);
     return e == cudaSuccess ? kTcOk : kTcErrCuda;
 }
 
 }  // namespace
+
+TcWorkspace::~TcWorkspace() {
+    if (partials) cudaFree(partials);
+    if (flags) cudaFree(flags);
+}
+
+TcLaunchInfo tc_gemm_last_launch() { return g_last; }
 
 int tc_gemm_stages(const TcGemmConfig& c) {
 #define FI_STAGES(CG, BN, SK)                                          \
@@ -168,11 +238,17 @@ int tc_gemm_check(const TcGemmConfig& c, int M, int N, int K) {
     return kTcOk;
 }
 
-int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream) {
+TcLaunchInfo tc_gemm_plan(const TcGemmConfig& cfg, const TcGemmProblem& p) {
+    g_last = TcLaunchInfo{};
+    tc_gemm_launch(cfg, p, nullptr, true);
+    return g_last;
+}
+
+int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream, bool dry_run) {
     int chk = tc_gemm_check(cfg, p.M, p.N, p.K);
     if (chk != kTcOk) return chk;
 #define FI_LAUNCH(CG, BN, SK) \
-    if (cfg.cta_group == CG && cfg.bn == BN && cfg.split_k == SK) return launch_impl<CG, BN, SK>(cfg, p, stream);
+    if (cfg.cta_group == CG && cfg.bn == BN && cfg.split_k == SK) return launch_impl<CG, BN, SK>(cfg, p, stream, dry_run);
     FI_LAUNCH(1, 64, 1) FI_LAUNCH(1, 128, 1) FI_LAUNCH(1, 256, 1)
     FI_LAUNCH(2, 128, 1) FI_LAUNCH(2, 256, 1)
     FI_LAUNCH(1, 64, 2) FI_LAUNCH(1, 128, 2) FI_LAUNCH(1, 128, 4) FI_LAUNCH(1, 256, 2) FI_LAUNCH(1, 256, 4) FI_LAUNCH(2, 256, 2) FI_LAUNCH(2, 256, 4) FI_LAUNCH(2, 128, 2) FI_LAUNCH(2, 128, 4)

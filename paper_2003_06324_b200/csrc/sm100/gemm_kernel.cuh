@@ -1,7 +1,7 @@
 // Warp-specialised, persistent tcgen05 GEMM: the sm_100a lowering of the
 // Fireiron tensor-core strategy
 //
-//   tile BMxBN .to block [.pair]           -> persistent CTA (pair) tile loop
+//   tile BMxBN .to block [.pair]           -> persistent CTA (pair) work loop
 //   [split K/S .splitk]                    -> S CTAs of a cluster share a tile
 //   epilog tm { init {TMEM_ZERO} store {tile 32 BN .to warp; TMEM_STORE} }
 //   split 64 .stages S                     -> S-deep TMA/MMA mbarrier ring
@@ -10,15 +10,26 @@
 //
 // Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (leader CTA),
 // warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM -> RF -> GL).
-// Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps
-// the main loop of tile i+1. With kCtaGroup == 2 a CTA pair (cluster of 2)
-// computes a 256xBN tile with tcgen05.mma.cta_group::2: each CTA stages its
-// 128 rows of A and BN/2 rows of B; the accumulator rows stay in each CTA's
-// TMEM. Split-K (kSplitK > 1) gives each CTA (pair) of a cluster a K slice of
-// the same output tile; the partial accumulators are published in shared
-// memory (reusing the drained operand ring) and reduced through DSMEM in a
-// fixed rank order (so results are deterministic) before the fused epilog
-// store. Cluster rank = split_rank * kCtaGroup + pair_rank.
+// Accumulators are double-buffered in TMEM so the epilogue of one work unit
+// overlaps the main loop of the next. With kCtaGroup == 2 a CTA pair (cluster
+// of 2) computes a 256xBN tile with tcgen05.mma.cta_group::2: each CTA stages
+// its 128 rows of A and BN/2 rows of B; the accumulator rows stay in each
+// CTA's TMEM.
+//
+// Work distribution (which K-blocks of which tile a cluster computes):
+//  * data-parallel: whole tiles, round-robin over the persistent clusters;
+//  * stream-K (args.streamk): the T*KB (tile, K-block) iterations are cut into
+//    one contiguous range per cluster, so every SM does the same work and the
+//    wave-quantisation tail disappears. A tile cut by range boundaries is
+//    finished by the cluster owning its K prefix (its last work unit); every
+//    later K segment is a cluster's first unit and is published as an fp32
+//    partial in a global workspace slot + epoch flag. The owner adds the
+//    partials in K order, so results are deterministic;
+//  * cluster split-K (kSplitK > 1): the S CTAs (pairs) of a cluster own K
+//    slices of the same tile; partial accumulators are published in shared
+//    memory (reusing the drained operand ring) and reduced through DSMEM in a
+//    fixed rank order before the fused epilog store. Cluster rank =
+//    split_rank * kCtaGroup + pair_rank.
 #pragma once
 
 #include <cuda.h>
@@ -36,7 +47,7 @@ struct GemmArgs {
     long ldc = 0;               // elements
     int M = 0, N = 0, K = 0;
     int tiles_m = 0, tiles_n = 0;
-    int k_blocks = 0;           // 64-wide K blocks per work unit (K / 64 / splits)
+    int k_blocks = 0;           // 64-wide K blocks per tile (per split-K rank)
     int ab_format = 0;          // 0 = f16, 1 = bf16 (UMMA a/b format field)
     int a_mn_major = 0;         // A stored M-contiguous (col-major M x K)
     int b_mn_major = 0;         // B stored N-contiguous (row-major K x N)
@@ -45,6 +56,11 @@ struct GemmArgs {
     int group_m = 8;            // raster band (tile rows) for the default order
     int stages = 0;             // pipeline depth actually used (0 = deepest that fits)
     const int* tile_order = nullptr;  // optional permutation: Fireiron block-swizzle table
+    // stream-K
+    int streamk = 0;
+    float* workspace = nullptr;      // [clusters][kCtaGroup][BN][128] fp32 partials
+    unsigned* flags = nullptr;       // [clusters][kCtaGroup] epoch of the published partial
+    unsigned epoch = 0;              // this launch's epoch (> every earlier launch's)
 };
 
 template <int kCtaGroup, int BN, int kSplitK>
@@ -74,6 +90,7 @@ struct GemmShape {
     static_assert(RED_BYTES <= RING_BYTES, "split-K scratch must fit in the operand ring");
     static constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + 1024;  // + align slack
     static constexpr int kThreads = 256;
+    static constexpr int WS_FLOATS = BN * BM;     // one CTA's partial tile
 };
 
 // Tile id -> (tile row, tile col). With an explicit order table (the strategy's
@@ -94,6 +111,53 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, i
     if (rows > a.group_m) rows = a.group_m;
     tm = g * a.group_m + local % rows;
     tn = local / rows;
+}
+
+// One work unit: K-blocks [k0, k1) of tile `tile`.
+struct Unit {
+    int tile, k0, k1;
+};
+
+// The unit sequence of one cluster. Data-parallel: tiles cluster, cluster+P, ...
+// Stream-K: the contiguous iteration range [c*I/P, (c+1)*I/P) cut at tile edges.
+struct UnitIter {
+    long long it, end;  // stream-K iteration cursor
+    int t, step;        // data-parallel tile cursor
+    int kb, tiles;
+    bool sk;
+
+    __device__ UnitIter(const GemmArgs& a, int cluster, int nclusters) {
+        kb = a.k_blocks;
+        tiles = a.tiles_m * a.tiles_n;
+        sk = a.streamk != 0;
+        const long long total = static_cast<long long>(tiles) * kb;
+        it = total * cluster / nclusters;
+        end = total * (cluster + 1) / nclusters;
+        t = cluster;
+        step = nclusters;
+    }
+    __device__ bool next(Unit& u) {
+        if (!sk) {
+            if (t >= tiles) return false;
+            u = Unit{t, 0, kb};
+            t += step;
+            return true;
+        }
+        if (it >= end) return false;
+        u.tile = static_cast<int>(it / kb);
+        u.k0 = static_cast<int>(it - static_cast<long long>(u.tile) * kb);
+        const long long rem = end - it;
+        u.k1 = rem < kb - u.k0 ? u.k0 + static_cast<int>(rem) : kb;
+        it += u.k1 - u.k0;
+        return true;
+    }
+};
+
+// Last cluster whose stream-K range touches tile t (owner of its final K-block).
+__device__ __forceinline__ int sk_last_cluster(const GemmArgs& a, int t, int nclusters) {
+    const long long total = static_cast<long long>(a.tiles_m) * a.tiles_n * a.k_blocks;
+    const long long x = static_cast<long long>(t + 1) * a.k_blocks - 1;
+    return static_cast<int>(((x + 1) * nclusters - 1) / total);
 }
 
 template <typename T>
@@ -131,6 +195,17 @@ __device__ __forceinline__ void store_row32_any(const GemmArgs& a, int m, int n,
         case OutType::BF16: store_row32<__nv_bfloat16>(a, m, n, v); break;
     }
 }
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// bar.sync among the 4 epilogue warps only (named barrier 1, 128 threads)
+__device__ __forceinline__ void epilogue_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // Kernel body; the tensor maps must be __grid_constant__ kernel parameters
 // (TMA reads them through their parameter-space address).
@@ -188,7 +263,6 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     const uint32_t tmem_base = *tmem_slot;
 
     const int nst = (args.stages > 0 && args.stages < kStages) ? args.stages : kStages;
-    const int num_tiles = args.tiles_m * args.tiles_n;
     const int cluster = blockIdx.x / kClusterSize;
     const int nclusters = gridDim.x / kClusterSize;
     const int kb0 = static_cast<int>(split_rank) * args.k_blocks;  // first K block of my slice
@@ -199,18 +273,21 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
-            for (int t = cluster; t < num_tiles; t += nclusters, ++it) {
+            UnitIter units(args, cluster, nclusters);
+            Unit u;
+            while (units.next(u)) {
                 int tm, tn;
-                tile_coords(args, t, tm, tn);
+                tile_coords(args, u.tile, tm, tn);
                 if constexpr (kSplitK > 1) {
                     // the ring doubles as the reduction scratch: wait until every
                     // peer has read my previous partial tile
                     mbar_wait_cluster(rempty_bar, (static_cast<uint32_t>(it) & 1) ^ 1);
                     fence_proxy_async();
                 }
+                ++it;
                 const int m0 = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
                 const int n0 = tn * BN + static_cast<int>(pair_rank) * S::BN_LOCAL;
-                for (int kb = 0; kb < args.k_blocks; ++kb) {
+                for (int kb = u.k0; kb < u.k1; ++kb) {
                     mbar_wait(&empty_bar[s], ph ^ 1);
                     uint8_t* sa = ring + s * S::STAGE_BYTES;
                     uint8_t* sb = sa + S::A_BYTES;
@@ -255,13 +332,16 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
-            for (int t = cluster; t < num_tiles; t += nclusters, ++it) {
+            UnitIter units(args, cluster, nclusters);
+            Unit u;
+            while (units.next(u)) {
                 const int buf = it & 1;
                 const uint32_t use = static_cast<uint32_t>(it >> 1);
+                ++it;
                 mbar_wait_cluster(&tempty_bar[buf], (use & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
-                for (int kb = 0; kb < args.k_blocks; ++kb) {
+                for (int kb = u.k0; kb < u.k1; ++kb) {
                     mbar_wait(&full_bar[s], ph);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(ring + s * S::STAGE_BYTES);
@@ -270,7 +350,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     for (int k = 0; k < S::BK / 16; ++k) {
                         uint64_t ad = smem_desc_sw128(sa + k * a_kstep, a_lbo, 1024);
                         uint64_t bd = smem_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
-                        umma_f16<kCtaGroup>(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                        umma_f16<kCtaGroup>(d_tmem, ad, bd, idesc, (kb > u.k0 || k > 0) ? 1u : 0u);
                     }
                     if constexpr (kCtaGroup == 1) umma_commit(&empty_bar[s]);
                     else umma_commit_pair(&empty_bar[s], pair_mask);
@@ -285,17 +365,26 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         const int q = warp - 4;  // TMEM lane quarter owned by this warp
         const int row = q * 32 + lane;
         int it = 0;
-        for (int t = cluster; t < num_tiles; t += nclusters, ++it) {
+        UnitIter units(args, cluster, nclusters);
+        Unit u;
+        const int kb = args.k_blocks;
+        float* my_ws = args.workspace + static_cast<long>(cluster * kCtaGroup + pair_rank) * S::WS_FLOATS;
+        while (units.next(u)) {
             int tm, tn;
-            tile_coords(args, t, tm, tn);
+            tile_coords(args, u.tile, tm, tn);
             const int buf = it & 1;
             const uint32_t use = static_cast<uint32_t>(it >> 1);
+            const uint32_t tile_use = static_cast<uint32_t>(it);
+            ++it;
             mbar_wait(&tfull_bar[buf], use & 1);
             tc_fence_after();
             const int m = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM + row;
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                    static_cast<uint32_t>(buf * BN);
             if constexpr (kSplitK == 1) {
+                const bool full = u.k0 == 0 && u.k1 == kb;
+                const bool writer = u.k0 > 0;  // later K segment: publish a partial
+                const int last = (!full && !writer) ? sk_last_cluster(args, u.tile, nclusters) : cluster;
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t r[32];
@@ -304,6 +393,23 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     float v[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                    if (writer) {
+                        // workspace slot [col][row]: per-column stores are coalesced
+                        float* w = my_ws + (c * 32) * S::BM + row;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) w[j * S::BM] = v[j];
+                        continue;
+                    }
+                    // fixup owner: add the later K segments' partials in K order
+                    for (int p = cluster + 1; p <= last; ++p) {
+                        const unsigned* flag = args.flags + (p * kCtaGroup + pair_rank);
+                        while (ld_acquire_gpu(flag) < args.epoch) __nanosleep(64);
+                        const float* w = args.workspace +
+                                         static_cast<long>(p * kCtaGroup + pair_rank) * S::WS_FLOATS +
+                                         (c * 32) * S::BM + row;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] += __ldcg(w + j * S::BM);
+                    }
                     store_row32_any(args, m, tn * BN + c * 32, v);
                 }
                 tc_fence_before();
@@ -312,8 +418,14 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     if constexpr (kCtaGroup == 1) mbar_arrive(&tempty_bar[buf]);
                     else mbar_arrive_cluster(&tempty_bar[buf], crank - pair_rank);
                 }
+                if (writer) {
+                    // all four epilogue warps have stored their rows: publish
+                    __threadfence();
+                    epilogue_bar();
+                    if (q == 0 && lane == 0)
+                        st_release_gpu(args.flags + (cluster * kCtaGroup + pair_rank), args.epoch);
+                }
             } else {
-                const uint32_t tile_use = static_cast<uint32_t>(it);
                 // The producer only refills the ring after rempty completes, and
                 // tfull implies this tile's operands are consumed: the ring is free.
                 float* my_row = red + row * S::RED_LD;

@@ -25,6 +25,8 @@ struct TcGemmConfig {
     int stages = 0;      // pipeline depth (0 = deepest that fits in shared memory)
 };
 
+struct TcWorkspace;
+
 struct TcGemmProblem {
     const void* A = nullptr;
     const void* B = nullptr;
@@ -34,12 +36,33 @@ struct TcGemmProblem {
     const int* tile_order = nullptr; // device array, tiles_m*tiles_n entries, or null
     int num_sms = 148;
     int max_ctas = 0;                // 0 = persistent over all SMs
+    int streamk = -1;                // -1 auto (when the data-parallel tail wastes >5%), 0 off, 1 on
+    // stream-K partial workspace; null = a library-owned pool. Launches that
+    // share a workspace must be ordered on one stream.
+    TcWorkspace* workspace = nullptr;
 };
+
+// Device workspace of the stream-K fixup: one fp32 partial tile per CTA
+// (clusters x cta_group x BN x 128) + one epoch flag per CTA.
+struct TcWorkspace {
+    float* partials = nullptr;
+    unsigned* flags = nullptr;
+    size_t partial_floats = 0, flag_count = 0;
+    unsigned epoch = 0;  // incremented by every launch that uses it
+    ~TcWorkspace();
+};
+
+struct TcLaunchInfo {
+    int ctas = 0, clusters = 0, streamk = 0;
+};
+TcLaunchInfo tc_gemm_last_launch();
 
 int tc_gemm_check(const TcGemmConfig& c, int M, int N, int K);
 int tc_gemm_stages(const TcGemmConfig& c);
 int tc_gemm_smem_bytes(const TcGemmConfig& c);
 int tc_gemm_tmem_cols(const TcGemmConfig& c);
-int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream);
+int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream, bool dry_run = false);
+// Grid / scheduling decision of a launch without launching (needs the device).
+TcLaunchInfo tc_gemm_plan(const TcGemmConfig& cfg, const TcGemmProblem& p);
 
 }  // namespace fireiron::sm100

@@ -1,0 +1,86 @@
+"""Multi-GPU execution of a Fireiron GEMM strategy, sharded by M/N output
+blocks across the GPUs of one node (BASELINE.json configs[4]).
+
+Partitioning (1-D over N): with g ranks, rank r owns
+  A_r  = A[r*M/g:(r+1)*M/g, :]     (row shard, never communicated)
+  B_r  = B[:, r*N/g:(r+1)*N/g]     (column shard, contiguous in col-major B)
+and computes the row band C_r = A_r * B (M/g x N). B is all-gathered over
+NVLink with NCCL as g per-owner broadcasts; the GEMM of column chunk j starts
+as soon as chunk j has arrived, so the collective overlaps the tensor-core
+work chunk by chunk (the own chunk needs no communication and runs first).
+
+Each chunk GEMM is the same tcgen05 strategy on the (M/g) x (N/g) x K shard
+shape; column chunks of col-major B and C are contiguous, so chunk j is a
+plain pointer offset.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, List
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    m: int           # global
+    n: int
+    k: int
+    m_local: int     # rows of A / C owned by this rank
+    n_chunk: int     # columns per B chunk (one per owner rank)
+
+    @property
+    def a_elems(self) -> int:
+        return self.m_local * self.k
+
+    @property
+    def b_chunk_elems(self) -> int:
+        return self.k * self.n_chunk
+
+    @property
+    def c_elems(self) -> int:
+        return self.m_local * self.n
+
+    def b_chunk_offset(self, j: int) -> int:
+        """Element offset of owner j's chunk in the gathered col-major B (K x N)."""
+        return j * self.b_chunk_elems
+
+    def c_chunk_offset(self, j: int) -> int:
+        """Element offset of column chunk j in the col-major C band (M/g x N)."""
+        return j * self.m_local * self.n_chunk
+
+    def order(self) -> List[int]:
+        """Chunk compute order: own chunk first, then the others as they land."""
+        return [self.rank] + [j for j in range(self.world) if j != self.rank]
+
+
+def make_shard(m: int, n: int, k: int, world: int, rank: int, tile_m: int = 256, tile_n: int = 256) -> Shard:
+    if m % world or n % world:
+        raise ValueError(f"{m}x{n} does not split over {world} ranks")
+    ml, nc = m // world, n // world
+    if ml % tile_m or nc % tile_n:
+        raise ValueError(f"shard {ml}x{nc} is not a multiple of the {tile_m}x{tile_n} block tile")
+    return Shard(rank, world, m, n, k, ml, nc)
+
+
+def sharded_step(shard: Shard, a_local, b_local, b_full, c_local, gemm: Callable, dist, stream_wait=None):
+    """One step: broadcast every owner's B chunk into b_full (async, NCCL
+    queues them in order) and run the chunk GEMMs as chunks arrive.
+
+    gemm(j, a_local, b_chunk_view, c_chunk_view) launches chunk j.
+    b_full is a flat buffer of K*N elements; b_local is this rank's chunk.
+    Works for any torch.distributed backend (nccl on GPUs, gloo in tests)."""
+    me = shard.rank
+    off = shard.b_chunk_offset(me)
+    b_full[off:off + shard.b_chunk_elems].copy_(b_local)
+    works = {}
+    for j in range(shard.world):
+        o = shard.b_chunk_offset(j)
+        works[j] = dist.broadcast(b_full[o:o + shard.b_chunk_elems], src=j, async_op=True)
+    for j in shard.order():
+        if j != me:
+            works[j].wait()  # stream-ordered on NCCL: the GEMM waits only for chunk j
+        bo, co = shard.b_chunk_offset(j), shard.c_chunk_offset(j)
+        gemm(j, a_local, b_full[bo:bo + shard.b_chunk_elems],
+             c_local[co:co + shard.m_local * shard.n_chunk])
+    works[me].wait()

@@ -115,6 +115,64 @@ done
 """
 
 
+def wmma_decomp(m: int, n: int, k: int) -> str:
+    """The paper's staged WMMA strategy (transcribed as in
+    SURVEY.md Appendix A.6): CTA 128x128, K chunks of 128 staged GL->SH with
+    padded tiles, warp 64x32 tiles of 16x16 fragments, WMMA leaves, epilog in
+    FR stored through a reused SH buffer. It is the reference simulator's
+    tensor-core analogue of the tcgen05 strategy (its CPU baseline arm)."""
+    return f"""spec MatMul({m},{n},{k})(GL,GL,GL)(Kernel) elems f16 f16 f32
+
+tile 128 128 .to block
+epilog fr {{
+  init {{
+    tile 64 32 .to warp
+    tile 16 16 .unroll
+    done
+  }}
+  store {{
+    load src sh .reusebuffer {{
+      tile 64 32 .to warp
+      tile 16 16 .unroll
+      done
+    }}
+    tile 16 128 .to warp
+    tile 1 128 .unroll
+    tile 1 4 .to thread
+    tile 1 1
+    done
+  }}
+}}
+split 128 .sync
+load a sh .pad 8 .nosync {{
+  tile 16 128 .to warp
+  tile 2 128 .unroll
+  tile 1 8 .to thread
+  tile 1 1
+  done
+}}
+load b sh .pad 8 {{
+  tile 128 16 .to warp
+  tile 128 2 .unroll
+  tile 8 1 .to thread .layout colmajor
+  tile 1 1
+  done
+}}
+tile 64 32 .to warp
+split 16 .unroll
+load a fr {{
+  tile 16 16 .unroll
+  done
+}}
+load b fr {{
+  tile 16 16 .unroll
+  done
+}}
+tile 16 16 .unroll
+done
+"""
+
+
 # The BASELINE.json configurations
 def c2_strategy() -> str:
     """configs[1]: 4096^3 f16 in / f32 acc, GL->SH (TMA) -> TMEM (tcgen05), 1 B200."""

@@ -122,3 +122,34 @@ def test_unsupported_tile_reports_cleanly(fi):
     with pytest.raises(fi.FiError) as e:
         fi.Plan(s)
     assert e.value.kind in ("Unsupported", "NonDivisible")
+
+
+@pytest.mark.parametrize("pair,tile_n", [(True, 256), (False, 128), (True, 128)])
+@pytest.mark.parametrize("shape", [(1280, 1024, 2048), (2048, 2048, 16384)])
+def test_streamk_partitioning_exact_and_deterministic(fi, oracle, monkeypatch, pair, tile_n, shape):
+    """Stream-K cuts tiles across clusters (fixup chains of several K segments):
+    integer inputs stay exact, uniform inputs are bitwise reproducible."""
+    monkeypatch.setenv("FI_STREAMK", "1")
+    m, n, k = shape
+    s = fi.strategies.tc_strategy(m, n, k, pair=pair, tile_n=tile_n)
+    plan = fi.Plan(s)
+    assert plan.info.streamk == 1
+    a = oracle.fill(m, k, 11, True)
+    b = oracle.fill(k, n, 12, True)
+    c = plan.run_host(a, b)
+    rng = np.random.default_rng(3)
+    rows, cols = rng.integers(0, m, 4096), rng.integers(0, n, 4096)
+    ar, br = oracle.round_elem(a, "f16"), oracle.round_elem(b, "f16")
+    assert np.array_equal(c[rows, cols].astype(np.float64), oracle.sample_f64(ar, br, rows, cols))
+    assert np.array_equal(c, np.round(c))
+    a = oracle.fill(m, k, 13, False)
+    b = oracle.fill(k, n, 14, False)
+    c1, c2 = plan.run_host(a, b), plan.run_host(a, b)
+    assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
+    want = oracle.sample_f64(oracle.round_elem(a, "f16"), oracle.round_elem(b, "f16"), rows, cols)
+    assert np.max(np.abs(c1[rows, cols] - want)) / np.max(np.abs(want)) <= TOL_NORMWISE
+
+
+def test_c2_plan_uses_streamk(fi):
+    plan = fi.Plan(fi.strategies.c2_strategy())
+    assert plan.info.streamk == 1 and plan.info.launch_ctas == 148
