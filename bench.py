@@ -74,7 +74,7 @@ class ClockSampler:
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
 
-    def __init__(self, device_index=0, period=0.005):
+    def __init__(self, device_index=0, period=0.001):
         self.samples, self.reasons, self.period = [], set(), period
         self.max_mhz = None
         self._stop = threading.Event()

@@ -77,9 +77,10 @@ class Plan:
         self.info = info
 
     def close(self):
-        if getattr(self, "_h", None):
-            N.lib.fi_plan_destroy(self._h)
-            self._h = None
+        h = getattr(self, "_h", None)
+        self._h = None
+        if h and N is not None and getattr(N, "lib", None) is not None:
+            N.lib.fi_plan_destroy(h)
 
     __del__ = close
 

@@ -138,23 +138,27 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         max_active = n;
     }
     if (clusters > max_active) clusters = max_active;
-    // data-parallel when whole tiles fill the waves well, stream-K otherwise
+    // Tail split: whole waves data-parallel; the R leftover tiles of the partial
+    // last wave are cut into S K-slices so the idle clusters share them.
+    // S <= P/R (one unit per cluster), slices of >= 8 K-blocks, S <= 6 (the
+    // fixup stages S-1 partial chunks, double-buffered, in the operand ring).
     const int kb = args.k_blocks;
-    int sk_clusters = clusters;
-    const long long sk_cap = static_cast<long long>(tiles) * (kb / 8 > 1 ? kb / 8 : 1);
-    if (sk_cap < sk_clusters) sk_clusters = static_cast<int>(sk_cap);
     const int dp_clusters = clusters < tiles ? clusters : tiles;
-    const int waves = (tiles + dp_clusters - 1) / dp_clusters;
-    const double dp_eff = static_cast<double>(tiles) / (static_cast<double>(waves) * clusters);
-    bool sk = kSplitK == 1 && sk_clusters > 1 &&
-              (p.streamk == 1 || (p.streamk < 0 && dp_eff < 0.95 && tiles % sk_clusters != 0));
+    const int full_waves = tiles / clusters;
+    const int rest = tiles - full_waves * clusters;
+    int slices = rest > 0 ? clusters / rest : 1;
+    if (slices > kb / 8) slices = kb / 8;
+    if (slices > 6) slices = 6;
+    if (p.streamk == 0 || kSplitK > 1) slices = 1;
+    const bool sk = slices >= 2;
     if (dry_run) {
-        const int c = sk ? sk_clusters : dp_clusters;
+        const int c = sk ? clusters : dp_clusters;
         g_last = TcLaunchInfo{c * kCluster, c, sk ? 1 : 0};
         return kTcOk;
     }
     if (sk) {
-        clusters = sk_clusters;
+        args.sk_tile_begin = full_waves * clusters;
+        args.sk_slices = slices;
         TcWorkspace* ws = p.workspace ? p.workspace : shared_workspace();
         const size_t need_p = static_cast<size_t>(clusters) * kCtaGroup * S::WS_FLOATS;
         const size_t need_f = static_cast<size_t>(clusters) * kCtaGroup;

@@ -18,13 +18,13 @@
 //
 // Work distribution (which K-blocks of which tile a cluster computes):
 //  * data-parallel: whole tiles, round-robin over the persistent clusters;
-//  * stream-K (args.streamk): the T*KB (tile, K-block) iterations are cut into
-//    one contiguous range per cluster, so every SM does the same work and the
-//    wave-quantisation tail disappears. A tile cut by range boundaries is
-//    finished by the cluster owning its K prefix (its last work unit); every
-//    later K segment is a cluster's first unit and is published as an fp32
-//    partial in a global workspace slot + epoch flag. The owner adds the
-//    partials in K order, so results are deterministic;
+//  * tail split (args.streamk): whole waves of tiles run data-parallel; the
+//    leftover tiles of the partial last wave are split into S K-slices at
+//    fixed offsets so the idle clusters share their work (a stream-K variant
+//    that keeps clusters in K lockstep: contiguous stream-K ranges measured 5x
+//    the DRAM traffic). Slices 1..S-1 publish fp32 partials (global workspace
+//    slot + epoch flag); slice 0 stages them into its idle operand ring with
+//    bulk copies and adds them in K order, so results are deterministic;
 //  * cluster split-K (kSplitK > 1): the S CTAs (pairs) of a cluster own K
 //    slices of the same tile; partial accumulators are published in shared
 //    memory (reusing the drained operand ring) and reduced through DSMEM in a
@@ -58,7 +58,9 @@ struct GemmArgs {
     const int* tile_order = nullptr;  // optional permutation: Fireiron block-swizzle table
     // stream-K
     int streamk = 0;
-    float* workspace = nullptr;      // [clusters][kCtaGroup][BN][128] fp32 partials
+    int sk_tile_begin = 0;           // tiles before this index run data-parallel
+    int sk_slices = 1;               // K-slices per leftover tile
+    float* workspace = nullptr;     // [clusters][kCtaGroup][BN][128] fp32 partials
     unsigned* flags = nullptr;       // [clusters][kCtaGroup] epoch of the published partial
     unsigned epoch = 0;              // this launch's epoch (> every earlier launch's)
 };
@@ -118,47 +120,42 @@ struct Unit {
     int tile, k0, k1;
 };
 
-// The unit sequence of one cluster. Data-parallel: tiles cluster, cluster+P, ...
-// Stream-K: the contiguous iteration range [c*I/P, (c+1)*I/P) cut at tile edges.
+// The unit sequence of one cluster. Tiles [0, D) run data-parallel (tile
+// cluster, cluster+P, ...: consecutive clusters work on neighbouring tiles and
+// advance through K in lockstep, so a wave's A/B panels are read once from
+// DRAM). The R = T - D leftover tiles (the partial last wave) are split into S
+// K-slices at fixed offsets: cluster c < R*S takes slice c / R of tile
+// D + c % R. Clusters in the same slice stay in K lockstep (L2 reuse again),
+// and slice 0 -- whose cluster also holds the K prefix -- owns the fixup.
 struct UnitIter {
-    long long it, end;  // stream-K iteration cursor
-    int t, step;        // data-parallel tile cursor
-    int kb, tiles;
-    bool sk;
+    int t, step, kb, dp_tiles, tail_unit;
+    int slices, rest;
 
     __device__ UnitIter(const GemmArgs& a, int cluster, int nclusters) {
         kb = a.k_blocks;
-        tiles = a.tiles_m * a.tiles_n;
-        sk = a.streamk != 0;
-        const long long total = static_cast<long long>(tiles) * kb;
-        it = total * cluster / nclusters;
-        end = total * (cluster + 1) / nclusters;
+        const int tiles = a.tiles_m * a.tiles_n;
+        slices = a.streamk ? a.sk_slices : 1;
+        dp_tiles = a.streamk ? a.sk_tile_begin : tiles;
+        rest = tiles - dp_tiles;
+        tail_unit = (a.streamk && cluster < rest * slices) ? cluster : -1;
         t = cluster;
         step = nclusters;
     }
     __device__ bool next(Unit& u) {
-        if (!sk) {
-            if (t >= tiles) return false;
+        if (t < dp_tiles) {
             u = Unit{t, 0, kb};
             t += step;
             return true;
         }
-        if (it >= end) return false;
-        u.tile = static_cast<int>(it / kb);
-        u.k0 = static_cast<int>(it - static_cast<long long>(u.tile) * kb);
-        const long long rem = end - it;
-        u.k1 = rem < kb - u.k0 ? u.k0 + static_cast<int>(rem) : kb;
-        it += u.k1 - u.k0;
+        if (tail_unit < 0) return false;
+        const int s = tail_unit / rest;
+        u.tile = dp_tiles + tail_unit % rest;
+        u.k0 = kb * s / slices;
+        u.k1 = kb * (s + 1) / slices;
+        tail_unit = -1;
         return true;
     }
 };
-
-// Last cluster whose stream-K range touches tile t (owner of its final K-block).
-__device__ __forceinline__ int sk_last_cluster(const GemmArgs& a, int t, int nclusters) {
-    const long long total = static_cast<long long>(a.tiles_m) * a.tiles_n * a.k_blocks;
-    const long long x = static_cast<long long>(t + 1) * a.k_blocks - 1;
-    return static_cast<int>(((x + 1) * nclusters - 1) / total);
-}
 
 template <typename T>
 __device__ __forceinline__ T cvt_out(float v);
@@ -229,7 +226,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     uint64_t* tempty_bar = bars + 2 * kStages + 2;  // [2] epilogue -> MMA
     uint64_t* rfull_bar = bars + 2 * kStages + 4;   // split-K: all partials published
     uint64_t* rempty_bar = bars + 2 * kStages + 5;  // split-K: all peers done reading
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
+    uint64_t* stage_bar = bars + 2 * kStages + 6;   // [2] stream-K fixup staging
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 8);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -250,6 +248,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         }
         mbar_init(rfull_bar, 4 * kSplitK);
         mbar_init(rempty_bar, 4 * kSplitK);
+        mbar_init(&stage_bar[0], 1);
+        mbar_init(&stage_bar[1], 1);
         fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
@@ -384,7 +384,31 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             if constexpr (kSplitK == 1) {
                 const bool full = u.k0 == 0 && u.k1 == kb;
                 const bool writer = u.k0 > 0;  // later K segment: publish a partial
-                const int last = (!full && !writer) ? sk_last_cluster(args, u.tile, nclusters) : cluster;
+                const int rest = args.tiles_m * args.tiles_n - args.sk_tile_begin;  // tail tiles
+                const int nparts = (!full && !writer) ? args.sk_slices - 1 : 0;   // slices 1..S-1
+                // Fixup owner (the cluster's last unit: the ring is idle): one
+                // thread acquires the later segments' flags, then their 32-column
+                // chunks are staged into the ring by bulk copies, double-buffered.
+                constexpr uint32_t kChunkBytes = 32 * S::BM * 4;
+                auto stage = [&](int c) {
+                    float* dst = reinterpret_cast<float*>(ring) + static_cast<long>((c & 1) * nparts) * 32 * S::BM;
+                    mbar_arrive_expect_tx(&stage_bar[c & 1], kChunkBytes * nparts);
+                    for (int p = 0; p < nparts; ++p)
+                        bulk_copy_g2s(dst + p * 32 * S::BM,
+                                      args.workspace +
+                                          static_cast<long>((cluster + (p + 1) * rest) * kCtaGroup + pair_rank) * S::WS_FLOATS +
+                                          static_cast<long>(c) * 32 * S::BM,
+                                      kChunkBytes, &stage_bar[c & 1]);
+                };
+                if (nparts > 0 && q == 0 && lane == 0) {
+                    for (int p = 1; p <= nparts; ++p) {
+                        const unsigned* flag = args.flags + ((cluster + p * rest) * kCtaGroup + pair_rank);
+                        while (ld_acquire_gpu(flag) < args.epoch) __nanosleep(32);
+                    }
+                    fence_proxy_async();
+                    stage(0);
+                    if (BN / 32 > 1) stage(1);
+                }
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t r[32];
@@ -400,15 +424,20 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                         for (int j = 0; j < 32; ++j) w[j * S::BM] = v[j];
                         continue;
                     }
-                    // fixup owner: add the later K segments' partials in K order
-                    for (int p = cluster + 1; p <= last; ++p) {
-                        const unsigned* flag = args.flags + (p * kCtaGroup + pair_rank);
-                        while (ld_acquire_gpu(flag) < args.epoch) __nanosleep(64);
-                        const float* w = args.workspace +
-                                         static_cast<long>(p * kCtaGroup + pair_rank) * S::WS_FLOATS +
-                                         (c * 32) * S::BM + row;
+                    if (nparts > 0) {
+                        // add the later K segments' partials in K order
+                        mbar_wait(&stage_bar[c & 1], (static_cast<uint32_t>(c) >> 1) & 1);
+                        const float* src = reinterpret_cast<const float*>(ring) +
+                                           static_cast<long>((c & 1) * nparts) * 32 * S::BM + row;
+                        for (int p = 0; p < nparts; ++p) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] += __ldcg(w + j * S::BM);
+                            for (int j = 0; j < 32; ++j) v[j] += src[(p * 32 + j) * S::BM];
+                        }
+                        if (c + 2 < BN / 32) {  // refill this buffer with chunk c + 2
+                            fence_proxy_async();
+                            epilogue_bar();
+                            if (q == 0 && lane == 0) stage(c + 2);
+                        }
                     }
                     store_row32_any(args, m, tn * BN + c * 32, v);
                 }

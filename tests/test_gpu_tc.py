@@ -124,12 +124,13 @@ def test_unsupported_tile_reports_cleanly(fi):
     assert e.value.kind in ("Unsupported", "NonDivisible")
 
 
-@pytest.mark.parametrize("pair,tile_n", [(True, 256), (False, 128), (True, 128)])
-@pytest.mark.parametrize("shape", [(1280, 1024, 2048), (2048, 2048, 16384)])
-def test_streamk_partitioning_exact_and_deterministic(fi, oracle, monkeypatch, pair, tile_n, shape):
-    """Stream-K cuts tiles across clusters (fixup chains of several K segments):
-    integer inputs stay exact, uniform inputs are bitwise reproducible."""
-    monkeypatch.setenv("FI_STREAMK", "1")
+@pytest.mark.parametrize("pair,tile_n,shape", [(True, 256, (1280, 1024, 2048)), (False, 128, (1280, 1024, 2048)),
+                                               (True, 256, (1024, 1024, 32768)), (True, 128, (4096, 4096, 4096)),
+                                               (False, 256, (4096, 4096, 4096)), (True, 256, (4096, 4096, 4096))])
+def test_tail_split_exact_and_deterministic(fi, oracle, monkeypatch, pair, tile_n, shape):
+    """The partial last wave's tiles are split into K-slices across idle
+    clusters (fixups of up to 6 slices): integer inputs stay exact, uniform
+    inputs are bitwise reproducible and within tolerance."""
     m, n, k = shape
     s = fi.strategies.tc_strategy(m, n, k, pair=pair, tile_n=tile_n)
     plan = fi.Plan(s)
@@ -150,6 +151,6 @@ def test_streamk_partitioning_exact_and_deterministic(fi, oracle, monkeypatch, p
     assert np.max(np.abs(c1[rows, cols] - want)) / np.max(np.abs(want)) <= TOL_NORMWISE
 
 
-def test_c2_plan_uses_streamk(fi):
+def test_c2_plan_uses_tail_split(fi):
     plan = fi.Plan(fi.strategies.c2_strategy())
     assert plan.info.streamk == 1 and plan.info.launch_ctas == 148
