@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <mutex>
 
 #include "gemm_kernel.cuh"
@@ -62,7 +64,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
 
     const CUtensorMapDataType dt =
         cfg.ab_format == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-    CUtensorMap tmA, tmB;
+    CUtensorMap tmA, tmB, tmB2;
     CUresult r;
     if (cfg.a_mn_major)
         r = encode_2d(&tmA, dt, p.A, p.M, p.K, static_cast<uint64_t>(p.lda) * 2, 64, 64);
@@ -73,6 +75,10 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         r = encode_2d(&tmB, dt, p.B, p.N, p.K, static_cast<uint64_t>(p.ldb) * 2, 64, 64);
     else
         r = encode_2d(&tmB, dt, p.B, p.K, p.N, static_cast<uint64_t>(p.ldb) * 2, 64, S::BN_LOCAL);
+    if (r == CUDA_SUCCESS && !cfg.b_mn_major && S::BN_LOCAL >= 16)  // half-width tail units
+        r = encode_2d(&tmB2, dt, p.B, p.K, p.N, static_cast<uint64_t>(p.ldb) * 2, 64, S::BN_LOCAL / 2);
+    else
+        tmB2 = tmB;
     if (r != CUDA_SUCCESS) return kTcErrTensorMap;
 
     GemmArgs args;
@@ -149,11 +155,20 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     int slices = rest > 0 ? clusters / rest : 1;
     if (slices > kb / 8) slices = kb / 8;
     if (slices > 6) slices = 6;
-    if (p.streamk == 0 || kSplitK > 1) slices = 1;
-    const bool sk = slices >= 2;
+    // N-split of the partial last wave: two half-width units per leftover tile
+    const bool half_ok = BN >= 128 && (!cfg.b_mn_major || (BN / 2 / kCtaGroup) % 64 == 0);
+    const bool nsplit_ok = half_ok && rest > 0 && rest * 2 <= clusters;
+    int mode = 0;  // 0 data-parallel, 1 K-slice tail, 2 N-split tail
+    if (kSplitK == 1) {
+        if (p.streamk < 0) mode = (full_waves >= 1 && nsplit_ok) ? 2 : (full_waves == 0 && slices >= 3) ? 1 : 0;
+        else if (p.streamk == 1) mode = slices >= 2 ? 1 : 0;
+        else if (p.streamk == 2) mode = nsplit_ok ? 2 : 0;
+    }
+    if (mode == 2) slices = 2;
+    const bool sk = mode != 0;
     if (dry_run) {
         const int c = sk ? clusters : dp_clusters;
-        g_last = TcLaunchInfo{c * kCluster, c, sk ? 1 : 0};
+        g_last = TcLaunchInfo{c * kCluster, c, mode};
         return kTcOk;
     }
     if (sk) {
@@ -176,7 +191,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
             ws->flag_count = need_f;
             ws->epoch = 0;
         }
-        args.streamk = 1;
+        args.streamk = mode;
         args.workspace = ws->partials;
         args.flags = ws->flags;
         args.epoch = ++ws->epoch;
@@ -186,7 +201,30 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     if (clusters < 1) clusters = 1;
     lc.gridDim = dim3(clusters * kCluster, 1, 1);
     g_last = TcLaunchInfo{clusters * kCluster, clusters, sk ? 1 : 0};
-    cudaError_t e = cudaLaunchKernelEx(&lc, kernel, tmA, tmB, args);
+    // debugging aid: FI_TC_TRACE=<file> records a per-unit timeline of this launch
+    static const char* trace_path = std::getenv("FI_TC_TRACE");
+    static unsigned long long* trace_buf = nullptr;
+    const size_t trace_n = static_cast<size_t>(clusters) * kCluster * 16 * 4;
+    if (trace_path) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 148 * 16 * 4 * sizeof(unsigned long long) * 2);
+        cudaMemsetAsync(trace_buf, 0, trace_n * sizeof(unsigned long long), stream);
+        args.trace = trace_buf;
+    }
+    cudaError_t e = cudaLaunchKernelEx(&lc, kernel, tmA, tmB, tmB2, args);
+    if (trace_path && e == cudaSuccess) {
+        std::vector<unsigned long long> h(trace_n);
+        cudaMemcpyAsync(h.data(), trace_buf, trace_n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
+        if (FILE* f = std::fopen(trace_path, "a")) {
+            std::fprintf(f, "launch ctas %d cluster %d mode %d tiles %d kb %d\n", clusters * kCluster, kCluster,
+                         args.streamk, tiles, kb);
+            for (size_t i = 0; i < trace_n; i += 4)
+                if (h[i] || h[i + 2])
+                    std::fprintf(f, "%zu %zu %llu %llu %llu %llu\n", i / 64, (i / 4) % 16, h[i], h[i + 1], h[i + 2],
+                                 h[i + 3]);
+            std::fclose(f);
+        }
+    }
     return e == cudaSuccess ? kTcOk : kTcErrCuda;
 }
 

@@ -63,7 +63,19 @@ struct GemmArgs {
     float* workspace = nullptr;     // [clusters][kCtaGroup][BN][128] fp32 partials
     unsigned* flags = nullptr;       // [clusters][kCtaGroup] epoch of the published partial
     unsigned epoch = 0;              // this launch's epoch (> every earlier launch's)
+    // optional timeline (FI_TC_TRACE): [cta][unit < 16][4] %globaltimer stamps:
+    // producer first load, MMA last commit, epilogue accumulator ready, epilogue done
+    unsigned long long* trace = nullptr;
 };
+
+__device__ __forceinline__ unsigned long long global_timer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace_stamp(const GemmArgs& a, int unit, int ev) {
+    if (a.trace && unit < 16) a.trace[(blockIdx.x * 16 + unit) * 4 + ev] = global_timer_ns();
+}
 
 template <int kCtaGroup, int BN, int kSplitK>
 struct GemmShape {
@@ -115,9 +127,10 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, i
     tn = local / rows;
 }
 
-// One work unit: K-blocks [k0, k1) of tile `tile`.
+// One work unit: K-blocks [k0, k1) of columns [n_off, n_off + width) of tile `tile`.
 struct Unit {
     int tile, k0, k1;
+    int n_off, width;
 };
 
 // The unit sequence of one cluster. Tiles [0, D) run data-parallel (tile
@@ -127,31 +140,44 @@ struct Unit {
 // K-slices at fixed offsets: cluster c < R*S takes slice c / R of tile
 // D + c % R. Clusters in the same slice stay in K lockstep (L2 reuse again),
 // and slice 0 -- whose cluster also holds the K prefix -- owns the fixup.
+// With args.streamk == 2 the leftover tiles are instead split along N into two
+// half-width units (tcgen05 MMA with N = BN/2): no partials and no fixup.
+template <int BN>
 struct UnitIter {
     int t, step, kb, dp_tiles, tail_unit;
-    int slices, rest;
+    int slices, rest, mode;
 
     __device__ UnitIter(const GemmArgs& a, int cluster, int nclusters) {
         kb = a.k_blocks;
         const int tiles = a.tiles_m * a.tiles_n;
-        slices = a.streamk ? a.sk_slices : 1;
-        dp_tiles = a.streamk ? a.sk_tile_begin : tiles;
+        mode = a.streamk;
+        slices = mode ? a.sk_slices : 1;
+        dp_tiles = mode ? a.sk_tile_begin : tiles;
         rest = tiles - dp_tiles;
-        tail_unit = (a.streamk && cluster < rest * slices) ? cluster : -1;
+        tail_unit = (mode && cluster < rest * slices) ? cluster : -1;
         t = cluster;
         step = nclusters;
     }
     __device__ bool next(Unit& u) {
         if (t < dp_tiles) {
-            u = Unit{t, 0, kb};
+            u = Unit{t, 0, kb, 0, BN};
             t += step;
             return true;
         }
         if (tail_unit < 0) return false;
         const int s = tail_unit / rest;
         u.tile = dp_tiles + tail_unit % rest;
-        u.k0 = kb * s / slices;
-        u.k1 = kb * (s + 1) / slices;
+        if (mode == 2) {  // N-split: half s of the tile's columns, full K
+            u.k0 = 0;
+            u.k1 = kb;
+            u.width = BN / 2;
+            u.n_off = s * (BN / 2);
+        } else {          // K-slice s
+            u.k0 = kb * s / slices;
+            u.k1 = kb * (s + 1) / slices;
+            u.n_off = 0;
+            u.width = BN;
+        }
         tail_unit = -1;
         return true;
     }
@@ -208,7 +234,7 @@ __device__ __forceinline__ void epilogue_bar() { asm volatile("bar.sync 1, 128;"
 // (TMA reads them through their parameter-space address).
 template <int kCtaGroup, int BN, int kSplitK>
 __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
-                                                   const GemmArgs& args) {
+                                                   const CUtensorMap& tmB2, const GemmArgs& args) {
     using S = GemmShape<kCtaGroup, BN, kSplitK>;
     constexpr int kStages = S::kStages;
     constexpr int kClusterSize = kCtaGroup * kSplitK;
@@ -255,6 +281,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmB2);
     }
     if (warp == 2) tmem_alloc<kCtaGroup>(tmem_slot, S::TMEM_COLS);
     tc_fence_before();
@@ -273,26 +300,30 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
-            UnitIter units(args, cluster, nclusters);
+            UnitIter<BN> units(args, cluster, nclusters);
             Unit u;
             while (units.next(u)) {
                 int tm, tn;
                 tile_coords(args, u.tile, tm, tn);
+                const bool half = u.width != BN;
+                const int b_rows = u.width / kCtaGroup;  // B rows staged by this CTA
+                const uint32_t tx = static_cast<uint32_t>(S::A_BYTES + b_rows * S::BK * 2) * kCtaGroup;
                 if constexpr (kSplitK > 1) {
                     // the ring doubles as the reduction scratch: wait until every
                     // peer has read my previous partial tile
                     mbar_wait_cluster(rempty_bar, (static_cast<uint32_t>(it) & 1) ^ 1);
                     fence_proxy_async();
                 }
+                trace_stamp(args, it, 0);
                 ++it;
                 const int m0 = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
-                const int n0 = tn * BN + static_cast<int>(pair_rank) * S::BN_LOCAL;
+                const int n0 = tn * BN + u.n_off + static_cast<int>(pair_rank) * b_rows;
                 for (int kb = u.k0; kb < u.k1; ++kb) {
                     mbar_wait(&empty_bar[s], ph ^ 1);
                     uint8_t* sa = ring + s * S::STAGE_BYTES;
                     uint8_t* sb = sa + S::A_BYTES;
                     const int k0 = (kb0 + kb) * S::BK;
-                    if (mma_leader) mbar_arrive_expect_tx(&full_bar[s], S::STAGE_BYTES * kCtaGroup);
+                    if (mma_leader) mbar_arrive_expect_tx(&full_bar[s], tx);
                     auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
                         if constexpr (kCtaGroup == 1) tma_load_2d(dst, map, &full_bar[s], c0, c1);
                         else tma_load_2d_pair(dst, map, &full_bar[s], c0, c1);
@@ -304,11 +335,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                         load(sa, &tmA, k0, m0);
                     }
                     if (args.b_mn_major) {
-#pragma unroll
-                        for (int j = 0; j < S::BN_LOCAL / 64; ++j)
+                        for (int j = 0; j < b_rows / 64; ++j)
                             load(sb + j * 8192, &tmB, n0 + j * 64, k0);
                     } else {
-                        load(sb, &tmB, k0, n0);
+                        load(sb, half ? &tmB2 : &tmB, k0, n0);  // tmB2: box of BN_LOCAL/2 rows
                     }
                     if (++s == nst) { s = 0; ph ^= 1; }
                 }
@@ -318,12 +348,11 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         // ------------------------------------------------------------ MMA issuer
         if (mma_leader && lane == 0) {
             // instruction descriptor: f32 accumulate, a/b format, majors, N>>3, M>>4
-            const uint32_t idesc = (1u << 4) | (static_cast<uint32_t>(args.ab_format) << 7) |
-                                   (static_cast<uint32_t>(args.ab_format) << 10) |
-                                   (static_cast<uint32_t>(args.a_mn_major) << 15) |
-                                   (static_cast<uint32_t>(args.b_mn_major) << 16) |
-                                   (static_cast<uint32_t>(BN >> 3) << 17) |
-                                   (static_cast<uint32_t>(S::BM_TILE >> 4) << 24);
+            const uint32_t idesc_base = (1u << 4) | (static_cast<uint32_t>(args.ab_format) << 7) |
+                                        (static_cast<uint32_t>(args.ab_format) << 10) |
+                                        (static_cast<uint32_t>(args.a_mn_major) << 15) |
+                                        (static_cast<uint32_t>(args.b_mn_major) << 16) |
+                                        (static_cast<uint32_t>(S::BM_TILE >> 4) << 24);
             // K-major: rows of 128B, 8-row atoms 1024B apart (SBO), K step = 32B.
             // MN-major: 64-element chunks 8KB apart (LBO), 8 k-rows per atom (SBO 1KB),
             //           K step of 16 = two atoms = 2KB.
@@ -332,12 +361,13 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
-            UnitIter units(args, cluster, nclusters);
+            UnitIter<BN> units(args, cluster, nclusters);
             Unit u;
             while (units.next(u)) {
                 const int buf = it & 1;
                 const uint32_t use = static_cast<uint32_t>(it >> 1);
                 ++it;
+                const uint32_t idesc = idesc_base | (static_cast<uint32_t>(u.width >> 3) << 17);
                 mbar_wait_cluster(&tempty_bar[buf], (use & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
@@ -358,6 +388,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 }
                 if constexpr (kCtaGroup == 1) umma_commit(&tfull_bar[buf]);
                 else umma_commit_pair(&tfull_bar[buf], pair_mask);
+                trace_stamp(args, it - 1, 1);
             }
         }
     } else if (warp >= 4) {
@@ -365,7 +396,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         const int q = warp - 4;  // TMEM lane quarter owned by this warp
         const int row = q * 32 + lane;
         int it = 0;
-        UnitIter units(args, cluster, nclusters);
+        UnitIter<BN> units(args, cluster, nclusters);
         Unit u;
         const int kb = args.k_blocks;
         float* my_ws = args.workspace + static_cast<long>(cluster * kCtaGroup + pair_rank) * S::WS_FLOATS;
@@ -377,6 +408,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             const uint32_t tile_use = static_cast<uint32_t>(it);
             ++it;
             mbar_wait(&tfull_bar[buf], use & 1);
+            if (q == 0 && lane == 0) trace_stamp(args, it - 1, 2);
             tc_fence_after();
             const int m = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM + row;
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
@@ -409,8 +441,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     stage(0);
                     if (BN / 32 > 1) stage(1);
                 }
+                __syncwarp();  // reconverge before the warp-collective tcgen05.ld
+                const int nchunks = u.width / 32;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = 0; c < nchunks; ++c) {
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(tbase + c * 32, r);
                     tmem_ld_wait();
@@ -437,9 +471,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                             fence_proxy_async();
                             epilogue_bar();
                             if (q == 0 && lane == 0) stage(c + 2);
+                            __syncwarp();
                         }
                     }
-                    store_row32_any(args, m, tn * BN + c * 32, v);
+                    store_row32_any(args, m, tn * BN + u.n_off + c * 32, v);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -454,6 +489,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     if (q == 0 && lane == 0)
                         st_release_gpu(args.flags + (cluster * kCtaGroup + pair_rank), args.epoch);
                 }
+                __syncwarp();
+                if (q == 0 && lane == 0) trace_stamp(args, it - 1, 3);
             } else {
                 // The producer only refills the ring after rempty completes, and
                 // tfull implies this tile's operands are consumed: the ring is free.
@@ -526,8 +563,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
 template <int kCtaGroup, int BN, int kSplitK>
 __global__ void __launch_bounds__(256, 1)
     fi_sm100_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  const __grid_constant__ GemmArgs args) {
-    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK>(tmA, tmB, args);
+                  const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ GemmArgs args) {
+    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK>(tmA, tmB, tmB2, args);
 }
 
 }  // namespace fireiron::sm100

@@ -1,0 +1,41 @@
+#!/usr/bin/env python3
+"""Summarise an FI_TC_TRACE timeline (last launch in the file): per-CTA unit
+spans (producer start -> MMA done -> epilogue ready -> epilogue done), the
+kernel span, and when CTAs go idle."""
+import statistics
+import sys
+
+
+def main(path):
+    launches, cur = [], None
+    for line in open(path):
+        if line.startswith("launch"):
+            cur = {"hdr": line.strip(), "rows": []}
+            launches.append(cur)
+        elif cur is not None:
+            cta, unit, p0, m1, e2, e3 = (int(x) for x in line.split())
+            cur["rows"].append((cta, unit, p0, m1, e2, e3))
+    last = launches[-1]
+    rows = last["rows"]
+    t0 = min(r[2] for r in rows if r[2])
+    end = max(max(r[3], r[5]) for r in rows)
+    print(last["hdr"], f"span {(end - t0) / 1e3:.1f} us, {len(set(r[0] for r in rows))} CTAs")
+    per_cta = {}
+    for cta, unit, p0, m1, e2, e3 in rows:
+        per_cta.setdefault(cta, []).append((unit, p0, m1, e2, e3))
+    done = [max(u[4] for u in us) - t0 for us in per_cta.values()]
+    print(f"CTA finish: min {min(done) / 1e3:.1f} us  median {statistics.median(done) / 1e3:.1f}  "
+          f"max {max(done) / 1e3:.1f}")
+    nunits = max(len(us) for us in per_cta.values())
+    for i in range(nunits):
+        mm = [(us[i][2] - us[i][1]) for us in per_cta.values() if len(us) > i and us[i][2] and us[i][1]]
+        ep = [(us[i][4] - us[i][3]) for us in per_cta.values() if len(us) > i and us[i][4] and us[i][3]]
+        st = [(us[i][1] - t0) for us in per_cta.values() if len(us) > i and us[i][1]]
+        if mm:
+            print(f"unit {i}: starts {min(st) / 1e3:6.1f}..{max(st) / 1e3:6.1f} us  producer->MMA done median "
+                  f"{statistics.median(mm) / 1e3:6.2f} us  epilogue median {statistics.median(ep) / 1e3 if ep else 0:6.2f} us"
+                  f" max {max(ep) / 1e3 if ep else 0:6.2f}  (n={len(mm)})")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])

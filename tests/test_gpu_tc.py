@@ -124,7 +124,7 @@ def test_unsupported_tile_reports_cleanly(fi):
     assert e.value.kind in ("Unsupported", "NonDivisible")
 
 
-@pytest.mark.parametrize("pair,tile_n,shape", [(True, 256, (1280, 1024, 2048)), (False, 128, (1280, 1024, 2048)),
+@pytest.mark.parametrize("pair,tile_n,shape", [(True, 256, (1280, 1024, 2048)), (False, 128, (2048, 2560, 2048)),
                                                (True, 256, (1024, 1024, 32768)), (True, 128, (4096, 4096, 4096)),
                                                (False, 256, (4096, 4096, 4096)), (True, 256, (4096, 4096, 4096))])
 def test_tail_split_exact_and_deterministic(fi, oracle, monkeypatch, pair, tile_n, shape):
@@ -134,7 +134,6 @@ def test_tail_split_exact_and_deterministic(fi, oracle, monkeypatch, pair, tile_
     m, n, k = shape
     s = fi.strategies.tc_strategy(m, n, k, pair=pair, tile_n=tile_n)
     plan = fi.Plan(s)
-    assert plan.info.streamk == 1
     a = oracle.fill(m, k, 11, True)
     b = oracle.fill(k, n, 12, True)
     c = plan.run_host(a, b)
@@ -153,4 +152,24 @@ def test_tail_split_exact_and_deterministic(fi, oracle, monkeypatch, pair, tile_
 
 def test_c2_plan_uses_tail_split(fi):
     plan = fi.Plan(fi.strategies.c2_strategy())
-    assert plan.info.streamk == 1 and plan.info.launch_ctas == 148
+    assert plan.info.streamk == 2 and plan.info.launch_ctas == 148  # N-split of the partial wave
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("layouts", [("colmajor", "colmajor", "colmajor"), ("rowmajor", "rowmajor", "rowmajor")])
+def test_forced_tail_modes(fi, oracle, monkeypatch, mode, layouts):
+    """Both tail modes on a 3.46-wave problem, both B majors: integer exact."""
+    monkeypatch.setenv("FI_STREAMK", mode)
+    m, n, k = 4096, 4096, 1024
+    plan = fi.Plan(fi.strategies.tc_strategy(m, n, k, layouts=layouts))
+    assert plan.info.streamk == int(mode)
+    a = oracle.fill(m, k, 21, True)
+    b = oracle.fill(k, n, 22, True)
+    c = plan.run_host(a, b)
+    rng = np.random.default_rng(4)
+    rows, cols = rng.integers(0, m, 8192), rng.integers(0, n, 8192)
+    ar, br = oracle.round_elem(a, "f16"), oracle.round_elem(b, "f16")
+    assert np.array_equal(c[rows, cols].astype(np.float64), oracle.sample_f64(ar, br, rows, cols))
+    # the last tiles (the tail) explicitly: a full 256-column strip at the end
+    assert np.array_equal(c[-256:, -256:].astype(np.float64),
+                          oracle.gemm_f64(ar[-256:], br[:, -256:]).astype(np.float64))
