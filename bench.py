@@ -56,7 +56,7 @@ def workload_of(args, world):
     if w == "c2":
         return dict(name="c2_4096^3_f16_f32acc_tcgen05_pair256x256", m=4096, n=4096, k=4096, ab="f16")
     if w == "c3":
-        return dict(name="c3_1024x1024x32768_f16_splitk4_cta128x256", m=1024, n=1024, k=32768, ab="f16")
+        return dict(name="c3_1024x1024x32768_f16_splitk4_pair256x256", m=1024, n=1024, k=32768, ab="f16")
     if w == "c5":
         return dict(name="c5_16384^3_bf16_sharded_MN_allgatherB", m=16384, n=16384, k=16384, ab="bf16")
     raise SystemExit(f"unknown workload {w}")
@@ -272,7 +272,7 @@ def ours_multi(args, fi, torch, rank, world):
     wl = workload_of(args, world)
     m, n, k = wl["m"], wl["n"], wl["k"]
     shard = make_shard(m, n, k, world, rank)
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     dt = torch.float16 if wl["ab"] == "f16" else torch.bfloat16
     plan = fi.Plan(strategy_for(fi, wl, shard.m_local, shard.n_chunk, k), device=dev.index)
@@ -346,8 +346,10 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if args.impl == "ours":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
-            dist.init_process_group("nccl")
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count())
+            # FI_DIST_BACKEND=gloo runs the sharded driver with several ranks on one
+            # GPU (logic check only; the measured configuration is NCCL, 1 rank/GPU)
+            dist.init_process_group(os.environ.get("FI_DIST_BACKEND", "nccl"))
         else:
             dist.init_process_group("gloo")
     import paper_2003_06324_b200 as fi

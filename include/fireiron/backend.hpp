@@ -95,7 +95,8 @@ struct PlanInfo {
     long grid_x = 1, grid_y = 1, block_threads = 1;
     long launch_ctas = 0;
     int cluster = 1, stages = 0, tmem_cols = 0, cta_group = 1, tile_m = 0, tile_n = 0, split_k = 1;
-    int streamk = 0;  // tcgen05 plans: stream-K work partitioning in use
+    int streamk = 0;  // tcgen05 plans: 0 data-parallel, 1 K-sliced tail/split, 2 N-split tail
+    int splitk_global = 0;  // .splitk lowered to cross-cluster K slices (else DSMEM cluster)
     long shared_bytes = 0;
     double flops = 0.0;
     std::string entry_name;

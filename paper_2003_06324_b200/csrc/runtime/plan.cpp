@@ -336,12 +336,23 @@ std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const 
                "cudaMemcpy");
             p.tile_order = impl->d_tile_order;
         }
+        // `.splitk` lowering: on CTA pairs the K slices run on separate clusters
+        // (partials exchanged through L2, summed in shared memory in slice
+        // order) when every (tile, slice) fits one wave -- measured 1082 vs
+        // 799 TF for the in-cluster DSMEM reduction at 1024x1024x32768
+        // (profiles/round1/); otherwise the cluster/DSMEM reduction.
+        const long tiles = (root.m() / tc.tile_m) * (root.n() / tc.tile_n);
+        if (tc.split_k > 1 && tc.cta_group == 2 && tiles * tc.split_k <= p.num_sms / 2) {
+            c.split_k = 1;
+            p.force_slices = tc.split_k;
+            info.splitk_global = 1;
+        }
         info.kind = 1;
         info.cta_group = tc.cta_group;
         info.tile_m = tc.tile_m;
         info.tile_n = tc.tile_n;
         info.split_k = tc.split_k;
-        info.cluster = tc.cta_group * tc.split_k;
+        info.cluster = tc.cta_group * c.split_k;
         info.stages = sm100::tc_gemm_stages(c);
         info.tmem_cols = sm100::tc_gemm_tmem_cols(c);
         info.shared_bytes = sm100::tc_gemm_smem_bytes(c);

@@ -160,11 +160,24 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     const bool nsplit_ok = half_ok && rest > 0 && rest * 2 <= clusters;
     int mode = 0;  // 0 data-parallel, 1 K-slice tail, 2 N-split tail
     if (kSplitK == 1) {
-        if (p.streamk < 0) mode = (full_waves >= 1 && nsplit_ok) ? 2 : (full_waves == 0 && slices >= 3) ? 1 : 0;
+        // auto: K-slices when each slice still has >= 24 K-blocks to amortise
+        // the (parallel, ~5 us) fixup; otherwise N-split halves; else plain
+        // (measured at 4096^3 / 1024^2x32768 / 4096^2x1024, profiles/round1/)
+        if (p.streamk < 0)
+            mode = (slices >= 2 && kb / slices >= 24) ? 1 : (full_waves >= 1 && nsplit_ok) ? 2 : 0;
         else if (p.streamk == 1) mode = slices >= 2 ? 1 : 0;
         else if (p.streamk == 2) mode = nsplit_ok ? 2 : 0;
     }
     if (mode == 2) slices = 2;
+    // explicit split-K of every tile (a .splitk strategy on CTA pairs): all
+    // tiles are K-sliced across clusters, partials reduced in shared memory
+    int sk_begin = full_waves * clusters;
+    if (kSplitK == 1 && p.force_slices > 1) {
+        if (tiles * p.force_slices > clusters) return kTcErrShape;
+        mode = 1;
+        slices = p.force_slices;
+        sk_begin = 0;
+    }
     const bool sk = mode != 0;
     if (dry_run) {
         const int c = sk ? clusters : dp_clusters;
@@ -172,7 +185,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         return kTcOk;
     }
     if (sk) {
-        args.sk_tile_begin = full_waves * clusters;
+        args.sk_tile_begin = sk_begin;
         args.sk_slices = slices;
         TcWorkspace* ws = p.workspace ? p.workspace : shared_workspace();
         const size_t need_p = static_cast<size_t>(clusters) * kCtaGroup * S::WS_FLOATS;
@@ -202,11 +215,11 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     lc.gridDim = dim3(clusters * kCluster, 1, 1);
     g_last = TcLaunchInfo{clusters * kCluster, clusters, sk ? 1 : 0};
     // debugging aid: FI_TC_TRACE=<file> records a per-unit timeline of this launch
-    static const char* trace_path = std::getenv("FI_TC_TRACE");
+    const char* trace_path = std::getenv("FI_TC_TRACE");
     static unsigned long long* trace_buf = nullptr;
-    const size_t trace_n = static_cast<size_t>(clusters) * kCluster * 16 * 4;
+    const size_t trace_n = static_cast<size_t>(clusters) * kCluster * 16 * 8;
     if (trace_path) {
-        if (!trace_buf) cudaMalloc(&trace_buf, 148 * 16 * 4 * sizeof(unsigned long long) * 2);
+        if (!trace_buf) cudaMalloc(&trace_buf, 148 * 16 * 8 * sizeof(unsigned long long));
         cudaMemsetAsync(trace_buf, 0, trace_n * sizeof(unsigned long long), stream);
         args.trace = trace_buf;
     }
@@ -218,10 +231,10 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         if (FILE* f = std::fopen(trace_path, "a")) {
             std::fprintf(f, "launch ctas %d cluster %d mode %d tiles %d kb %d\n", clusters * kCluster, kCluster,
                          args.streamk, tiles, kb);
-            for (size_t i = 0; i < trace_n; i += 4)
+            for (size_t i = 0; i < trace_n; i += 8)
                 if (h[i] || h[i + 2])
-                    std::fprintf(f, "%zu %zu %llu %llu %llu %llu\n", i / 64, (i / 4) % 16, h[i], h[i + 1], h[i + 2],
-                                 h[i + 3]);
+                    std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu\n", i / 128, (i / 8) % 16, h[i], h[i + 1],
+                                 h[i + 2], h[i + 3], h[i + 4], h[i + 5]);
             std::fclose(f);
         }
     }

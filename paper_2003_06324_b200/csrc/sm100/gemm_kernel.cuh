@@ -74,7 +74,10 @@ __device__ __forceinline__ unsigned long long global_timer_ns() {
     return t;
 }
 __device__ __forceinline__ void trace_stamp(const GemmArgs& a, int unit, int ev) {
-    if (a.trace && unit < 16) a.trace[(blockIdx.x * 16 + unit) * 4 + ev] = global_timer_ns();
+    if (a.trace && unit < 16) {
+        a.trace[(blockIdx.x * 16 + unit) * 8 + ev] = global_timer_ns();
+        a.trace[(blockIdx.x * 16 + unit) * 8 + 4 + ev] = clock64();  // SM clock: effective MHz
+    }
 }
 
 template <int kCtaGroup, int BN, int kSplitK>
@@ -131,6 +134,7 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, i
 struct Unit {
     int tile, k0, k1;
     int n_off, width;
+    int slice;  // K-slice index of a tail unit
 };
 
 // The unit sequence of one cluster. Tiles [0, D) run data-parallel (tile
@@ -160,13 +164,14 @@ struct UnitIter {
     }
     __device__ bool next(Unit& u) {
         if (t < dp_tiles) {
-            u = Unit{t, 0, kb, 0, BN};
+            u = Unit{t, 0, kb, 0, BN, 0};
             t += step;
             return true;
         }
         if (tail_unit < 0) return false;
         const int s = tail_unit / rest;
         u.tile = dp_tiles + tail_unit % rest;
+        u.slice = s;
         if (mode == 2) {  // N-split: half s of the tile's columns, full K
             u.k0 = 0;
             u.k1 = kb;
@@ -414,82 +419,96 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                    static_cast<uint32_t>(buf * BN);
             if constexpr (kSplitK == 1) {
-                const bool full = u.k0 == 0 && u.k1 == kb;
-                const bool writer = u.k0 > 0;  // later K segment: publish a partial
-                const int rest = args.tiles_m * args.tiles_n - args.sk_tile_begin;  // tail tiles
-                const int nparts = (!full && !writer) ? args.sk_slices - 1 : 0;   // slices 1..S-1
-                // Fixup owner (the cluster's last unit: the ring is idle): one
-                // thread acquires the later segments' flags, then their 32-column
-                // chunks are staged into the ring by bulk copies, double-buffered.
-                constexpr uint32_t kChunkBytes = 32 * S::BM * 4;
-                auto stage = [&](int c) {
-                    float* dst = reinterpret_cast<float*>(ring) + static_cast<long>((c & 1) * nparts) * 32 * S::BM;
-                    mbar_arrive_expect_tx(&stage_bar[c & 1], kChunkBytes * nparts);
-                    for (int p = 0; p < nparts; ++p)
-                        bulk_copy_g2s(dst + p * 32 * S::BM,
-                                      args.workspace +
-                                          static_cast<long>((cluster + (p + 1) * rest) * kCtaGroup + pair_rank) * S::WS_FLOATS +
-                                          static_cast<long>(c) * 32 * S::BM,
-                                      kChunkBytes, &stage_bar[c & 1]);
+                auto release_tmem = [&] {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (kCtaGroup == 1) mbar_arrive(&tempty_bar[buf]);
+                        else mbar_arrive_cluster(&tempty_bar[buf], crank - pair_rank);
+                    }
+                    __syncwarp();
                 };
-                if (nparts > 0 && q == 0 && lane == 0) {
-                    for (int p = 1; p <= nparts; ++p) {
-                        const unsigned* flag = args.flags + ((cluster + p * rest) * kCtaGroup + pair_rank);
-                        while (ld_acquire_gpu(flag) < args.epoch) __nanosleep(32);
-                    }
-                    fence_proxy_async();
-                    stage(0);
-                    if (BN / 32 > 1) stage(1);
-                }
-                __syncwarp();  // reconverge before the warp-collective tcgen05.ld
-                const int nchunks = u.width / 32;
+                if (u.k0 == 0 && u.k1 == kb) {
+                    // whole K range (a tile or an N-split half): TMEM -> RF -> GL
 #pragma unroll 1
-                for (int c = 0; c < nchunks; ++c) {
-                    uint32_t r[32];
-                    tmem_ld_32x32b_x32(tbase + c * 32, r);
-                    tmem_ld_wait();
-                    float v[32];
+                    for (int c = 0; c < u.width / 32; ++c) {
+                        uint32_t r[32];
+                        tmem_ld_32x32b_x32(tbase + c * 32, r);
+                        tmem_ld_wait();
+                        float v[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                    if (writer) {
-                        // workspace slot [col][row]: per-column stores are coalesced
-                        float* w = my_ws + (c * 32) * S::BM + row;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) w[j * S::BM] = v[j];
-                        continue;
+                        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                        store_row32_any(args, m, tn * BN + u.n_off + c * 32, v);
                     }
-                    if (nparts > 0) {
-                        // add the later K segments' partials in K order
-                        mbar_wait(&stage_bar[c & 1], (static_cast<uint32_t>(c) >> 1) & 1);
-                        const float* src = reinterpret_cast<const float*>(ring) +
-                                           static_cast<long>((c & 1) * nparts) * 32 * S::BM + row;
-                        for (int p = 0; p < nparts; ++p) {
+                    release_tmem();
+                } else {
+                    // K-slice tail unit (the cluster's last unit: its ring is idle).
+                    // Symmetric fixup: slice s owns 32-column chunks [c_lo, c_hi);
+                    // it keeps those in smem, publishes every other chunk in its
+                    // workspace slot, then sums its own range over all slices in
+                    // slice (= K) order and stores it: deterministic, and the S
+                    // slices' fixups run in parallel.
+                    const int nslc = args.sk_slices, s = u.slice;
+                    const int rest = args.tiles_m * args.tiles_n - args.sk_tile_begin;
+                    const int tile_idx = cluster % rest;
+                    constexpr int NCH = BN / 32;
+                    const int c_lo = NCH * s / nslc, c_hi = NCH * (s + 1) / nslc, nown = c_hi - c_lo;
+                    constexpr uint32_t kChunkFloats = 32 * S::BM;
+                    float* own = reinterpret_cast<float*>(ring);         // [nown][32][128]
+                    float* peer = own + nown * kChunkFloats;              // [slices][nown][32][128]
+#pragma unroll 1
+                    for (int c = 0; c < NCH; ++c) {
+                        uint32_t r[32];
+                        tmem_ld_32x32b_x32(tbase + c * 32, r);
+                        tmem_ld_wait();
+                        float* dst = (c >= c_lo && c < c_hi) ? own + (c - c_lo) * kChunkFloats + row
+                                                             : my_ws + c * kChunkFloats + row;
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) v[j] += src[(p * 32 + j) * S::BM];
-                        }
-                        if (c + 2 < BN / 32) {  // refill this buffer with chunk c + 2
-                            fence_proxy_async();
-                            epilogue_bar();
-                            if (q == 0 && lane == 0) stage(c + 2);
-                            __syncwarp();
-                        }
+                        for (int j = 0; j < 32; ++j) dst[j * S::BM] = __uint_as_float(r[j]);
                     }
-                    store_row32_any(args, m, tn * BN + u.n_off + c * 32, v);
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if constexpr (kCtaGroup == 1) mbar_arrive(&tempty_bar[buf]);
-                    else mbar_arrive_cluster(&tempty_bar[buf], crank - pair_rank);
-                }
-                if (writer) {
-                    // all four epilogue warps have stored their rows: publish
+                    release_tmem();
                     __threadfence();
-                    epilogue_bar();
-                    if (q == 0 && lane == 0)
+                    epilogue_bar();  // all rows of my partial are out
+                    if (q == 0 && lane == 0) {
                         st_release_gpu(args.flags + (cluster * kCtaGroup + pair_rank), args.epoch);
+                        if (nown > 0) {
+                            mbar_arrive_expect_tx(&stage_bar[0], (nslc - 1) * nown * kChunkFloats * 4);
+                            for (int j = 0; j < nslc; ++j) {
+                                if (j == s) continue;
+                                const int pc = tile_idx + j * rest;  // cluster of slice j
+                                while (ld_acquire_gpu(args.flags + (pc * kCtaGroup + pair_rank)) < args.epoch)
+                                    __nanosleep(32);
+                                fence_proxy_async();
+                                bulk_copy_g2s(peer + j * nown * kChunkFloats,
+                                              args.workspace +
+                                                  static_cast<long>(pc * kCtaGroup + pair_rank) * S::WS_FLOATS +
+                                                  static_cast<long>(c_lo) * kChunkFloats,
+                                              nown * kChunkFloats * 4, &stage_bar[0]);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (nown > 0) {
+                        mbar_wait(&stage_bar[0], 0);
+#pragma unroll 1
+                        for (int c = c_lo; c < c_hi; ++c) {
+                            float v[32];
+#pragma unroll 1
+                            for (int j = 0; j < nslc; ++j) {
+                                const float* src = (j == s ? own : peer + j * nown * kChunkFloats) +
+                                                   (c - c_lo) * kChunkFloats + row;
+                                if (j == 0) {
+#pragma unroll
+                                    for (int x = 0; x < 32; ++x) v[x] = src[x * S::BM];
+                                } else {
+#pragma unroll
+                                    for (int x = 0; x < 32; ++x) v[x] += src[x * S::BM];
+                                }
+                            }
+                            store_row32_any(args, m, tn * BN + c * 32, v);
+                        }
+                    }
                 }
-                __syncwarp();
                 if (q == 0 && lane == 0) trace_stamp(args, it - 1, 3);
             } else {
                 // The producer only refills the ring after rempty completes, and
@@ -548,6 +567,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 if (lane == 0)
                     for (int r = 0; r < kSplitK; ++r)
                         mbar_arrive_cluster(rempty_bar, static_cast<uint32_t>(r * kCtaGroup) + pair_rank);
+                __syncwarp();
+                if (q == 0 && lane == 0) trace_stamp(args, it - 1, 3);
             }
         }
     }

@@ -36,7 +36,8 @@ struct TcGemmProblem {
     const int* tile_order = nullptr; // device array, tiles_m*tiles_n entries, or null
     int num_sms = 148;
     int max_ctas = 0;                // 0 = persistent over all SMs
-    int streamk = -1;                // -1 auto (when the data-parallel tail wastes >5%), 0 off, 1 on
+    int streamk = -1;                // -1 auto, 0 data-parallel, 1 K-slice tail, 2 N-split tail
+    int force_slices = 0;            // >1: K-slice every tile into this many slices (.splitk on pairs)
     // stream-K partial workspace; null = a library-owned pool. Launches that
     // share a workspace must be ordered on one stream.
     TcWorkspace* workspace = nullptr;

@@ -182,7 +182,7 @@ def c2_strategy() -> str:
 def c3_strategy() -> str:
     """configs[2]: 1024x1024x32768 f16, in-kernel split-K with on-chip (DSMEM)
     reduction fused into the epilog."""
-    return tc_strategy(1024, 1024, 32768, pair=False, tile_n=256, split_k=4)
+    return tc_strategy(1024, 1024, 32768, pair=True, tile_n=256, split_k=4)
 
 
 def c5_strategy(m: int = 16384, n: int = 16384, k: int = 16384) -> str:

@@ -1,0 +1,20 @@
+"""Timelines of the C3 (1024x1024x32768) variants."""
+import os, sys
+sys.path.insert(0, ".")
+import torch
+import paper_2003_06324_b200 as fi
+A = torch.randn(1024 * 32768, device="cuda").half(); B = torch.randn(1024 * 32768, device="cuda").half()
+C = torch.empty(1024 * 1024, device="cuda")
+flush = torch.empty(128 << 20, device="cuda")
+s = torch.cuda.current_stream().cuda_stream
+for name, script, mode in [("pair_kslice", fi.strategies.tc_strategy(1024, 1024, 32768), "1"),
+                           ("c3_dsmem", fi.strategies.c3_strategy(), "0"),
+                           ("pair_dsmem2", fi.strategies.tc_strategy(1024, 1024, 32768, split_k=2), "0")]:
+    os.environ["FI_STREAMK"] = mode
+    plan = fi.Plan(script)
+    for _ in range(3): plan.launch(A.data_ptr(), B.data_ptr(), C.data_ptr(), s)
+    flush.zero_(); torch.cuda.synchronize()
+    os.environ["FI_TC_TRACE"] = f"gpurun_out/trace_c3_{name}.txt"
+    plan.launch(A.data_ptr(), B.data_ptr(), C.data_ptr(), s); torch.cuda.synchronize()
+    del os.environ["FI_TC_TRACE"]
+print("ok")

@@ -13,10 +13,15 @@ def main(path):
             cur = {"hdr": line.strip(), "rows": []}
             launches.append(cur)
         elif cur is not None:
-            cta, unit, p0, m1, e2, e3 = (int(x) for x in line.split())
-            cur["rows"].append((cta, unit, p0, m1, e2, e3))
+            vals = [int(x) for x in line.split()]
+            cur["rows"].append(tuple(vals[:6]))
+            if len(vals) >= 8 and vals[6] and vals[7] and vals[3] > vals[2]:
+                cur.setdefault("mhz", []).append((vals[7] - vals[6]) / (vals[3] - vals[2]) * 1e3)
     last = launches[-1]
     rows = last["rows"]
+    if last.get("mhz"):
+        print(f"effective SM clock (clock64 / globaltimer over MMA spans): median "
+              f"{statistics.median(last['mhz']):.0f} MHz, min {min(last['mhz']):.0f}, max {max(last['mhz']):.0f}")
     t0 = min(r[2] for r in rows if r[2])
     end = max(max(r[3], r[5]) for r in rows)
     print(last["hdr"], f"span {(end - t0) / 1e3:.1f} us, {len(set(r[0] for r in rows))} CTAs")

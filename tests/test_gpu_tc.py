@@ -152,7 +152,7 @@ def test_tail_split_exact_and_deterministic(fi, oracle, monkeypatch, pair, tile_
 
 def test_c2_plan_uses_tail_split(fi):
     plan = fi.Plan(fi.strategies.c2_strategy())
-    assert plan.info.streamk == 2 and plan.info.launch_ctas == 148  # N-split of the partial wave
+    assert plan.info.streamk == 1 and plan.info.launch_ctas == 148  # K-sliced partial wave
 
 
 @pytest.mark.parametrize("mode", ["1", "2"])
