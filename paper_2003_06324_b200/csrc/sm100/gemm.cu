@@ -36,7 +36,8 @@ EncodeTiledFn encode_tiled_fn() {
 }
 
 CUresult encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t d0,
-                   uint64_t d1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1) {
+                   uint64_t d1, uint64_t stride1_bytes, uint32_t box0, uint32_t box1,
+                   CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
     EncodeTiledFn encode = encode_tiled_fn();
     if (!encode) return CUDA_ERROR_NOT_INITIALIZED;
     cuuint64_t dims[2] = {d0, d1};
@@ -44,7 +45,7 @@ CUresult encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, u
     cuuint32_t box[2] = {box0, box1};
     cuuint32_t estr[2] = {1, 1};
     return encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
@@ -64,7 +65,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
 
     const CUtensorMapDataType dt =
         cfg.ab_format == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-    CUtensorMap tmA, tmB, tmB2;
+    CUtensorMap tmA, tmB, tmB2, tmC;
     CUresult r;
     if (cfg.a_mn_major)
         r = encode_2d(&tmA, dt, p.A, p.M, p.K, static_cast<uint64_t>(p.lda) * 2, 64, 64);
@@ -80,6 +81,22 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     else
         tmB2 = tmB;
     if (r != CUDA_SUCCESS) return kTcErrTensorMap;
+    // f32 column-major C: the epilogue stages 128x32 chunks in smem and stores
+    // them with one TMA bulk tensor store each (FI_TC_CSTORE=0 disables)
+    static const bool cstore_env = [] {
+        const char* v = std::getenv("FI_TC_CSTORE");
+        return !(v && v[0] == '0');
+    }();
+    const bool c_tma = cstore_env && kSplitK == 1 && cfg.out_type == 0 && !cfg.c_row_major &&
+                       (static_cast<uint64_t>(p.ldc) * 4) % 16 == 0 &&
+                       (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
+    if (c_tma) {
+        r = encode_2d(&tmC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p.C, p.M, p.N, static_cast<uint64_t>(p.ldc) * 4,
+                      S::BM, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (r != CUDA_SUCCESS) return kTcErrTensorMap;
+    } else {
+        tmC = tmA;  // unused
+    }
 
     GemmArgs args;
     args.C = p.C;
@@ -98,6 +115,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     args.group_m = cfg.group_m > 0 ? cfg.group_m : 8;
     args.tile_order = p.tile_order;
     args.stages = cfg.stages;
+    args.c_tma = c_tma ? 1 : 0;
 
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
@@ -223,7 +241,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         cudaMemsetAsync(trace_buf, 0, trace_n * sizeof(unsigned long long), stream);
         args.trace = trace_buf;
     }
-    cudaError_t e = cudaLaunchKernelEx(&lc, kernel, tmA, tmB, tmB2, args);
+    cudaError_t e = cudaLaunchKernelEx(&lc, kernel, tmA, tmB, tmB2, tmC, args);
     if (trace_path && e == cudaSuccess) {
         std::vector<unsigned long long> h(trace_n);
         cudaMemcpyAsync(h.data(), trace_buf, trace_n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);

@@ -60,6 +60,7 @@ struct GemmArgs {
     int streamk = 0;
     int sk_tile_begin = 0;           // tiles before this index run data-parallel
     int sk_slices = 1;               // K-slices per leftover tile
+    int c_tma = 0;                   // f32 col-major C stored by TMA from smem staging
     float* workspace = nullptr;     // [clusters][kCtaGroup][BN][128] fp32 partials
     unsigned* flags = nullptr;       // [clusters][kCtaGroup] epoch of the published partial
     unsigned epoch = 0;              // this launch's epoch (> every earlier launch's)
@@ -105,7 +106,11 @@ struct GemmShape {
     static constexpr int RING_BYTES = kStages * STAGE_BYTES;
     static constexpr int BAR_BYTES = 256;
     static_assert(RED_BYTES <= RING_BYTES, "split-K scratch must fit in the operand ring");
-    static constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + 1024;  // + align slack
+    // epilogue staging for TMA stores of C: two 32-column x 128-row fp32 chunks
+    static constexpr int EPI_CHUNK_BYTES = 32 * BM * 4;
+    static constexpr int EPI_BYTES = 2 * EPI_CHUNK_BYTES;
+    static constexpr int SMEM_BYTES = RING_BYTES + EPI_BYTES + BAR_BYTES + 1024;  // + align slack
+    static_assert(SMEM_BYTES <= 227 * 1024, "exceeds the sm_100a per-CTA shared memory");
     static constexpr int kThreads = 256;
     static constexpr int WS_FLOATS = BN * BM;     // one CTA's partial tile
 };
@@ -239,7 +244,8 @@ __device__ __forceinline__ void epilogue_bar() { asm volatile("bar.sync 1, 128;"
 // (TMA reads them through their parameter-space address).
 template <int kCtaGroup, int BN, int kSplitK>
 __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
-                                                   const CUtensorMap& tmB2, const GemmArgs& args) {
+                                                   const CUtensorMap& tmB2, const CUtensorMap& tmC,
+                                                   const GemmArgs& args) {
     using S = GemmShape<kCtaGroup, BN, kSplitK>;
     constexpr int kStages = S::kStages;
     constexpr int kClusterSize = kCtaGroup * kSplitK;
@@ -250,7 +256,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
     uint8_t* ring = smem;
     float* red = reinterpret_cast<float*>(ring);  // split-K scratch (ring reuse)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::RING_BYTES);
+    float* epi = reinterpret_cast<float*>(smem + S::RING_BYTES);  // [2][32 cols][128 rows] C staging
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::RING_BYTES + S::EPI_BYTES);
     uint64_t* full_bar = bars;                      // [kStages] TMA -> MMA
     uint64_t* empty_bar = bars + kStages;           // [kStages] MMA -> TMA
     uint64_t* tfull_bar = bars + 2 * kStages;       // [2] MMA -> epilogue
@@ -405,6 +412,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         Unit u;
         const int kb = args.k_blocks;
         float* my_ws = args.workspace + static_cast<long>(cluster * kCtaGroup + pair_rank) * S::WS_FLOATS;
+        uint32_t epi_chunk = 0;  // staged C chunks so far (alternating buffers)
         while (units.next(u)) {
             int tm, tn;
             tile_coords(args, u.tile, tm, tn);
@@ -428,7 +436,31 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     }
                     __syncwarp();
                 };
-                if (u.k0 == 0 && u.k1 == kb) {
+                if (u.k0 == 0 && u.k1 == kb && args.c_tma) {
+                    // whole K range, f32 col-major C: TMEM -> RF -> SMEM chunk -> TMA store.
+                    // Column j of a chunk is 128 contiguous rows (512 B): thread `row`
+                    // writes bank row % 32, conflict-free; one thread stores the chunk.
+                    const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
+#pragma unroll 1
+                    for (int c = 0; c < u.width / 32; ++c) {
+                        uint32_t r[32];
+                        tmem_ld_32x32b_x32(tbase + c * 32, r);
+                        float* stage = epi + (epi_chunk++ & 1) * (32 * S::BM);
+                        if (q == 0 && lane == 0) bulk_wait_group_read<1>();  // the store 2 chunks ago left it
+                        epilogue_bar();
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) stage[j * S::BM + row] = __uint_as_float(r[j]);
+                        fence_proxy_async();
+                        epilogue_bar();
+                        if (q == 0 && lane == 0) {
+                            tma_store_2d(&tmC, stage, m_cta, tn * BN + u.n_off + c * 32);
+                            bulk_commit_group();
+                        }
+                        __syncwarp();
+                    }
+                    release_tmem();
+                } else if (u.k0 == 0 && u.k1 == kb) {
                     // whole K range (a tile or an N-split half): TMEM -> RF -> GL
 #pragma unroll 1
                     for (int c = 0; c < u.width / 32; ++c) {
@@ -571,6 +603,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 if (q == 0 && lane == 0) trace_stamp(args, it - 1, 3);
             }
         }
+        if (q == 0 && lane == 0) bulk_wait_group<0>();  // TMA stores of C complete
+        __syncwarp();
     }
 
     tc_fence_before();
@@ -584,8 +618,9 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
 template <int kCtaGroup, int BN, int kSplitK>
 __global__ void __launch_bounds__(256, 1)
     fi_sm100_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ GemmArgs args) {
-    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK>(tmA, tmB, tmB2, args);
+                  const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
+                  const __grid_constant__ GemmArgs args) {
+    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK>(tmA, tmB, tmB2, tmC, args);
 }
 
 }  // namespace fireiron::sm100
