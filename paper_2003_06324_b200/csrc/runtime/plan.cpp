@@ -251,6 +251,9 @@ struct Plan::Impl {
     mutable size_t scratch_bytes = 0;
     mutable cudaStream_t own_stream = nullptr;
     mutable cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // pipelined run_host: copy-engine streams (H2D, D2H) and per-chunk events
+    mutable cudaStream_t up_stream = nullptr, down_stream = nullptr;
+    mutable std::vector<cudaEvent_t> pev;
 
     ~Impl() {
         if (module) {
@@ -262,6 +265,9 @@ struct Plan::Impl {
         if (d_tile_order) cudaFree(d_tile_order);
         if (scratch) cudaFree(scratch);
         if (own_stream) cudaStreamDestroy(own_stream);
+        if (up_stream) cudaStreamDestroy(up_stream);
+        if (down_stream) cudaStreamDestroy(down_stream);
+        for (cudaEvent_t e : pev) cudaEventDestroy(e);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
     }
@@ -269,6 +275,123 @@ struct Plan::Impl {
     const BufferDecl& root(int i) const { return prog.plan.at(i); }
     int out_root() const { return prog.root.is_matmul() ? 2 : 1; }
 };
+
+namespace {
+
+// ---------------------------------------------------------------- pipelined run_host
+// The host boundary moves fp32 matrices over PCIe (anvil::Matrix is fp32):
+// 4(MK + KN) bytes up and 4MN down, ~25x the GEMM's own time at 4096^3. For
+// tcgen05 plans with column-major B and C (Fireiron's default layouts) the
+// output is computed in column panels so the three engines overlap:
+//   up stream   : H2D A in pieces, then H2D B panel by panel
+//   main stream : snap A pieces to f16/bf16 as they land; per panel j: snap
+//                 B_j, GEMM on the (M x N/P x K) panel (pointer offsets into
+//                 the same TMA-described buffers), [widen C_j]
+//   down stream : D2H C_j while B_{j+1} is still coming up (PCIe is duplex)
+// Returns the number of panels P, or 0 when the plain path applies.
+int pipeline_chunks(const Plan::Impl& I) {
+    if (I.info.kind != 1 || !I.prog.root.is_matmul() || I.tp.tile_order) return 0;
+    if (I.tc.b_mn_major || I.tc.c_row_major) return 0;  // panels must be contiguous column ranges
+    if (const char* e = std::getenv("FI_HOST_PIPELINE"); e && e[0] == '0') return 0;
+    const long tiles_n = I.tp.N / I.tc.bn;
+    const double b_bytes = 4.0 * I.tp.K * I.tp.N;
+    int best = 0;
+    for (int p = 2; p <= 8; ++p)  // panels of >= 4 MiB each, whole block tiles
+        if (tiles_n % p == 0 && b_bytes / p >= 4.0 * (1 << 20)) best = p;
+    return best;
+}
+
+double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, float* C, cudaStream_t s,
+                          int chunks, char* base, const size_t* f32_in, const size_t* typed_in, size_t typed_c,
+                          size_t f32_c) {
+    if (!I.up_stream) {
+        ck(cudaStreamCreateWithFlags(&I.up_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&I.down_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+    constexpr int kAPieces = 4;
+    // events: [start][A pieces][B panels][C panels][gemm begin/end per panel][down done]
+    const size_t need = 1 + kAPieces + 2 * chunks + 2 * chunks + 1;
+    while (I.pev.size() < need) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        I.pev.push_back(e);
+    }
+    cudaEvent_t* ev = I.pev.data();
+    cudaEvent_t ev_start = ev[0], *ev_a = ev + 1, *ev_b = ev_a + kAPieces, *ev_c = ev_b + chunks;
+    cudaEvent_t *ev_g = ev_c + chunks, ev_down = ev_g[2 * chunks];
+    const BufferDecl& ra = I.root(0);
+    const BufferDecl& rb = I.root(1);
+    const BufferDecl& rc = I.root(2);
+    const int ea = elem_code(ra.elem), eb = elem_code(rb.elem), ec = elem_code(rc.elem);
+    const size_t wa = byte_width(ra.elem), wb = byte_width(rb.elem), wc = byte_width(rc.elem);
+    // scratch reuse across calls: the upload must not overtake earlier work on s
+    ck(cudaEventRecord(ev_start, s), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(I.up_stream, ev_start, 0), "cudaStreamWaitEvent");
+    ck(cudaStreamWaitEvent(I.down_stream, ev_start, 0), "cudaStreamWaitEvent");
+
+    // one storage range [e0, e1) of an input: H2D (into the f32 staging, or
+    // straight into the typed buffer for f32 roots), then snap on s
+    auto upload = [&](int which, const float* host, long e0, long e1, int elem, size_t w, cudaEvent_t done) {
+        if (e1 <= e0) {
+            ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
+            return;
+        }
+        char* typed = base + typed_in[which] + static_cast<size_t>(e0) * w;
+        float* stage = elem == 0 ? reinterpret_cast<float*>(typed)
+                                 : reinterpret_cast<float*>(base + f32_in[which]) + e0;
+        ck(cudaMemcpyAsync(stage, host + e0, static_cast<size_t>(e1 - e0) * 4, cudaMemcpyHostToDevice, I.up_stream),
+           "cudaMemcpyAsync");
+        ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(s, done, 0), "cudaStreamWaitEvent");
+        if (elem != 0)  // snapping to the root's element grid on ingestion (sim.hpp:507-510)
+            ck(rt::convert_f32(stage, typed, e1 - e0, elem, s), "input conversion");
+    };
+    const long a_ext = ra.extent();
+    for (int i = 0; i < kAPieces; ++i) {  // piece boundaries on 16-byte (4-element) multiples
+        const long e0 = (a_ext * i / kAPieces) & ~3L, e1 = i + 1 == kAPieces ? a_ext : (a_ext * (i + 1) / kAPieces) & ~3L;
+        upload(0, A, e0, e1, ea, wa, ev_a[i]);
+    }
+    const long nc = I.tp.N / chunks;  // columns per panel
+    const long b_ext = rb.extent(), c_ext = rc.extent();
+    float ms_total = 0.f;
+    for (int j = 0; j < chunks; ++j) {
+        const long b0 = j * nc * I.tp.ldb, b1 = j + 1 == chunks ? b_ext : (j + 1) * nc * I.tp.ldb;
+        upload(1, B, b0, b1, eb, wb, ev_b[j]);
+        sm100::TcGemmProblem p = I.tp;
+        p.workspace = &I.ws;
+        p.A = base + typed_in[0];
+        p.B = base + typed_in[1] + static_cast<size_t>(b0) * wb;
+        const long c0 = j * nc * I.tp.ldc, c1 = j + 1 == chunks ? c_ext : (j + 1) * nc * I.tp.ldc;
+        p.C = base + typed_c + static_cast<size_t>(c0) * wc;
+        p.N = static_cast<int>(nc);
+        ck(cudaEventRecord(ev_g[2 * j], s), "cudaEventRecord");
+        const int r = sm100::tc_gemm_launch(I.tc, p, s);
+        if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+        ck(cudaEventRecord(ev_g[2 * j + 1], s), "cudaEventRecord");
+        const float* result = reinterpret_cast<const float*>(base + typed_c) + c0;
+        if (ec != 0) {
+            float* wide = reinterpret_cast<float*>(base + f32_c) + c0;
+            ck(rt::widen_to_f32(base + typed_c + static_cast<size_t>(c0) * wc, wide, c1 - c0, ec, s),
+               "output conversion");
+            result = wide;
+        }
+        ck(cudaEventRecord(ev_c[j], s), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(I.down_stream, ev_c[j], 0), "cudaStreamWaitEvent");
+        ck(cudaMemcpyAsync(C + c0, result, static_cast<size_t>(c1 - c0) * 4, cudaMemcpyDeviceToHost, I.down_stream),
+           "cudaMemcpyAsync");
+    }
+    ck(cudaEventRecord(ev_down, I.down_stream), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(s, ev_down, 0), "cudaStreamWaitEvent");
+    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    for (int j = 0; j < chunks; ++j) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev_g[2 * j], ev_g[2 * j + 1]);
+        ms_total += ms;
+    }
+    return ms_total;
+}
+
+}  // namespace
 
 Plan::Plan(std::unique_ptr<Impl> impl) : impl_(std::move(impl)) {}
 Plan::~Plan() = default;
@@ -459,6 +582,12 @@ double Plan::run_host_raw(const float* A, const float* B, float* C, void* stream
         I.scratch_bytes = off;
     }
     auto* base = static_cast<char*>(I.scratch);
+    if (!I.ev0) {
+        ck(cudaEventCreate(&I.ev0), "cudaEventCreate");
+        ck(cudaEventCreate(&I.ev1), "cudaEventCreate");
+    }
+    if (const int chunks = pipeline_chunks(I); chunks > 0)
+        return run_host_pipelined(I, A, B, C, s, chunks, base, f32_in, typed_in, typed_c, f32_c);
     for (int i = 0; i < nin; ++i) {
         const BufferDecl& r = I.root(i);
         if (r.elem == ElemType::F32) {  // copy straight into the typed buffer
@@ -473,10 +602,6 @@ double Plan::run_host_raw(const float* A, const float* B, float* C, void* stream
         ck(rt::convert_f32(reinterpret_cast<float*>(base + f32_in[i]), base + typed_in[i], r.extent(),
                            elem_code(r.elem), s),
            "input conversion");
-    }
-    if (!I.ev0) {
-        ck(cudaEventCreate(&I.ev0), "cudaEventCreate");
-        ck(cudaEventCreate(&I.ev1), "cudaEventCreate");
     }
     ck(cudaEventRecord(I.ev0, s), "cudaEventRecord");
     launch(base + typed_in[0], nin > 1 ? base + typed_in[1] : nullptr, base + typed_c, s);
