@@ -67,7 +67,7 @@ typedef struct fi_plan_info {
     int64_t shared_bytes;         /* dynamic smem per CTA                       */
     double flops;                 /* 2*M*N*K (0 for Move)                       */
     int32_t streamk;              /* stream-K partitioning of (tile, K-block) work */
-    int32_t reserved;
+    int32_t remainder;            /* K-slice tail adds a remainder slice on idle clusters */
     char entry_name[128];
 } fi_plan_info;
 

@@ -58,7 +58,7 @@ class PlanInfo(C.Structure):
                 ("stages", C.c_int32), ("tmem_cols", C.c_int32), ("cta_group", C.c_int32),
                 ("tile_m", C.c_int32), ("tile_n", C.c_int32), ("split_k", C.c_int32),
                 ("shared_bytes", C.c_int64), ("flops", C.c_double), ("streamk", C.c_int32),
-                ("reserved", C.c_int32), ("entry_name", C.c_char * 128)]
+                ("remainder", C.c_int32), ("entry_name", C.c_char * 128)]
 
 
 def _load() -> C.CDLL:

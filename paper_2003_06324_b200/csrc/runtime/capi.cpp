@@ -127,6 +127,7 @@ fi_status fi_plan_query(fi_plan plan, fi_plan_info* info) {
         info->shared_bytes = pi.shared_bytes;
         info->flops = pi.flops;
         info->streamk = pi.streamk;
+        info->remainder = pi.remainder;
         std::strncpy(info->entry_name, pi.entry_name.c_str(), sizeof(info->entry_name) - 1);
         return FI_OK;
     });

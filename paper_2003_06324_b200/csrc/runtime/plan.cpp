@@ -388,6 +388,20 @@ double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, f
         cudaEventElapsedTime(&ms, ev_g[2 * j], ev_g[2 * j + 1]);
         ms_total += ms;
     }
+    if (std::getenv("FI_HOST_PIPELINE_TRACE")) {  // event timeline relative to the start (ms)
+        auto at = [&](cudaEvent_t e) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev_start, e);
+            return ms;
+        };
+        std::fprintf(stderr, "pipeline %d panels: A up", chunks);
+        for (int i = 0; i < kAPieces; ++i) std::fprintf(stderr, " %.3f", at(ev_a[i]));
+        std::fprintf(stderr, " | B up");
+        for (int j = 0; j < chunks; ++j) std::fprintf(stderr, " %.3f", at(ev_b[j]));
+        std::fprintf(stderr, " | gemm");
+        for (int j = 0; j < chunks; ++j) std::fprintf(stderr, " %.3f-%.3f", at(ev_g[2 * j]), at(ev_g[2 * j + 1]));
+        std::fprintf(stderr, " | C down done %.3f\n", at(ev_down));
+    }
     return ms_total;
 }
 
@@ -480,9 +494,11 @@ std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const 
         info.tmem_cols = sm100::tc_gemm_tmem_cols(c);
         info.shared_bytes = sm100::tc_gemm_smem_bytes(c);
         if (const char* e = std::getenv("FI_STREAMK")) p.streamk = std::atoi(e);
+        if (const char* e = std::getenv("FI_REMAINDER")) p.remainder = std::atoi(e);
         const sm100::TcLaunchInfo li = sm100::tc_gemm_plan(c, p);
         info.launch_ctas = li.ctas;
         info.streamk = li.streamk;
+        info.remainder = li.remainder;
         impl->source = generate(prog).source;
         return std::shared_ptr<Plan>(new Plan(std::move(impl)));
     }

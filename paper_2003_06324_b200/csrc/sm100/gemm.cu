@@ -116,6 +116,11 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     args.tile_order = p.tile_order;
     args.stages = cfg.stages;
     args.c_tma = c_tma ? 1 : 0;
+    static const bool ring_drain_env = [] {
+        const char* v = std::getenv("FI_TC_RING_DRAIN");
+        return !(v && v[0] == '0');
+    }();
+    args.ring_drain = ring_drain_env ? 1 : 0;
 
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
@@ -196,18 +201,47 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         slices = p.force_slices;
         sk_begin = 0;
     }
+    // Remainder slice: with E = clusters - R*S extra clusters, main slices
+    // get W = ceil(q*kb / (S*q + 1)) K-blocks and the remainder kb - S*W runs
+    // on the extra clusters, q = ceil(R/E) remainders each, so every cluster
+    // has ~q*kb/(S*q+1) blocks instead of kb/S (C3: 114 vs 128). Only when the
+    // remainder units stay long enough (>= 24 blocks) to hide their own
+    // epilogue and the owners' staging of S+1 sources fits in the ring.
+    int sk_w = 0, sk_extra = 0, sk_q = 0;
+    if (mode == 1 && p.remainder != 0) {
+        const int rest_tiles = tiles - sk_begin;
+        const int extra = clusters - rest_tiles * slices;
+        const int e = extra < rest_tiles ? extra : rest_tiles;
+        if (e > 0) {
+            const int q = (rest_tiles + e - 1) / e;
+            const int w = (q * kb + slices * q) / (slices * q + 1);
+            const int rk = kb - slices * w;
+            constexpr int NCH = BN / 32;
+            const int nown = (NCH + slices - 1) / slices;
+            const bool fits = (slices + 1) * nown * 32 * S::BM * 4 <= S::RING_BYTES;
+            if (fits && rk >= 24 && q * rk <= w && w * 100 <= (kb / slices) * 97) {
+                sk_w = w;
+                sk_extra = e;
+                sk_q = q;
+            }
+        }
+    }
     const bool sk = mode != 0;
     if (dry_run) {
         const int c = sk ? clusters : dp_clusters;
-        g_last = TcLaunchInfo{c * kCluster, c, mode};
+        g_last = TcLaunchInfo{c * kCluster, c, mode, sk_w > 0 ? 1 : 0};
         return kTcOk;
     }
     if (sk) {
         args.sk_tile_begin = sk_begin;
         args.sk_slices = slices;
+        args.sk_w = sk_w;
+        args.sk_extra = sk_extra;
+        args.sk_q = sk_q;
         TcWorkspace* ws = p.workspace ? p.workspace : shared_workspace();
-        const size_t need_p = static_cast<size_t>(clusters) * kCtaGroup * S::WS_FLOATS;
-        const size_t need_f = static_cast<size_t>(clusters) * kCtaGroup;
+        const size_t slots = static_cast<size_t>(clusters) + (sk_q > 1 ? static_cast<size_t>(sk_extra) * (sk_q - 1) : 0);
+        const size_t need_p = slots * kCtaGroup * S::WS_FLOATS;
+        const size_t need_f = slots * kCtaGroup;
         if (ws->partial_floats < need_p) {
             if (ws->partials) cudaFree(ws->partials);
             ws->partials = nullptr;
@@ -231,13 +265,13 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     }
     if (clusters < 1) clusters = 1;
     lc.gridDim = dim3(clusters * kCluster, 1, 1);
-    g_last = TcLaunchInfo{clusters * kCluster, clusters, sk ? 1 : 0};
+    g_last = TcLaunchInfo{clusters * kCluster, clusters, sk ? 1 : 0, sk_w > 0 ? 1 : 0};
     // debugging aid: FI_TC_TRACE=<file> records a per-unit timeline of this launch
     const char* trace_path = std::getenv("FI_TC_TRACE");
     static unsigned long long* trace_buf = nullptr;
-    const size_t trace_n = static_cast<size_t>(clusters) * kCluster * 16 * 8;
+    const size_t trace_n = static_cast<size_t>(clusters) * kCluster * 16 * 16;
     if (trace_path) {
-        if (!trace_buf) cudaMalloc(&trace_buf, 148 * 16 * 8 * sizeof(unsigned long long));
+        if (!trace_buf) cudaMalloc(&trace_buf, 148 * 16 * 16 * sizeof(unsigned long long));
         cudaMemsetAsync(trace_buf, 0, trace_n * sizeof(unsigned long long), stream);
         args.trace = trace_buf;
     }
@@ -249,10 +283,11 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         if (FILE* f = std::fopen(trace_path, "a")) {
             std::fprintf(f, "launch ctas %d cluster %d mode %d tiles %d kb %d\n", clusters * kCluster, kCluster,
                          args.streamk, tiles, kb);
-            for (size_t i = 0; i < trace_n; i += 8)
+            // cta unit t0 t1 t2 t3 clk0 clk1 t4 t5 t6 (globaltimer ns, clock64 of events 0/1)
+            for (size_t i = 0; i < trace_n; i += 16)
                 if (h[i] || h[i + 2])
-                    std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu\n", i / 128, (i / 8) % 16, h[i], h[i + 1],
-                                 h[i + 2], h[i + 3], h[i + 4], h[i + 5]);
+                    std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 256, (i / 16) % 16,
+                                 h[i], h[i + 1], h[i + 2], h[i + 3], h[i + 8], h[i + 9], h[i + 4], h[i + 5], h[i + 6]);
             std::fclose(f);
         }
     }

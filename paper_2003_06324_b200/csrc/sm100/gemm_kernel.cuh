@@ -60,12 +60,23 @@ struct GemmArgs {
     int streamk = 0;
     int sk_tile_begin = 0;           // tiles before this index run data-parallel
     int sk_slices = 1;               // K-slices per leftover tile
+    // remainder slices (K-slice tail only): main slice s covers K-blocks
+    // [s*sk_w, (s+1)*sk_w) and the remainder [sk_slices*sk_w, k_blocks) of
+    // leftover tile i runs on extra cluster rest*sk_slices + i % sk_extra as
+    // its (i / sk_extra)-th unit; sk_w = 0: even slices, no remainder
+    int sk_w = 0;
+    int sk_extra = 0;
+    int sk_q = 0;
     int c_tma = 0;                   // f32 col-major C stored by TMA from smem staging
-    float* workspace = nullptr;     // [clusters][kCtaGroup][BN][128] fp32 partials
-    unsigned* flags = nullptr;       // [clusters][kCtaGroup] epoch of the published partial
+    int ring_drain = 1;              // the cluster's last unit stages C in the idle operand ring
+    float* workspace = nullptr;     // [slots][kCtaGroup][BN][128] fp32 partials
+    unsigned* flags = nullptr;       // [slots][kCtaGroup] epoch of the published partial
+                                     // slots: one per cluster + sk_extra*(sk_q-1)
     unsigned epoch = 0;              // this launch's epoch (> every earlier launch's)
-    // optional timeline (FI_TC_TRACE): [cta][unit < 16][4] %globaltimer stamps:
-    // producer first load, MMA last commit, epilogue accumulator ready, epilogue done
+    // optional timeline (FI_TC_TRACE): [cta][unit < 16][16] %globaltimer stamps
+    // [0..7] and clock64 [8..15] of: producer first load, MMA last commit,
+    // epilogue accumulator ready, epilogue done, tail partial published, tail
+    // peers staged
     unsigned long long* trace = nullptr;
 };
 
@@ -76,8 +87,8 @@ __device__ __forceinline__ unsigned long long global_timer_ns() {
 }
 __device__ __forceinline__ void trace_stamp(const GemmArgs& a, int unit, int ev) {
     if (a.trace && unit < 16) {
-        a.trace[(blockIdx.x * 16 + unit) * 8 + ev] = global_timer_ns();
-        a.trace[(blockIdx.x * 16 + unit) * 8 + 4 + ev] = clock64();  // SM clock: effective MHz
+        a.trace[(blockIdx.x * 16 + unit) * 16 + ev] = global_timer_ns();
+        a.trace[(blockIdx.x * 16 + unit) * 16 + 8 + ev] = clock64();  // SM clock: effective MHz
     }
 }
 
@@ -139,8 +150,15 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, i
 struct Unit {
     int tile, k0, k1;
     int n_off, width;
-    int slice;  // K-slice index of a tail unit
+    int slice;  // K-slice index of a tail unit (sk_slices for a remainder)
+    int slot;   // workspace slot its partial is published in (tail units)
 };
+
+// Workspace slot of the remainder partial of leftover tile i.
+__device__ __forceinline__ int remainder_slot(const GemmArgs& a, int rest, int nclusters, int i) {
+    const int e = i % a.sk_extra, j = i / a.sk_extra;
+    return j == 0 ? rest * a.sk_slices + e : nclusters + e * (a.sk_q - 1) + j - 1;
+}
 
 // The unit sequence of one cluster. Tiles [0, D) run data-parallel (tile
 // cluster, cluster+P, ...: consecutive clusters work on neighbouring tiles and
@@ -154,16 +172,24 @@ struct Unit {
 template <int BN>
 struct UnitIter {
     int t, step, kb, dp_tiles, tail_unit;
-    int slices, rest, mode;
+    int slices, rest, mode, w;
+    int rem_e, rem_j, ncl;
+    const GemmArgs* args;
 
     __device__ UnitIter(const GemmArgs& a, int cluster, int nclusters) {
+        args = &a;
         kb = a.k_blocks;
         const int tiles = a.tiles_m * a.tiles_n;
         mode = a.streamk;
         slices = mode ? a.sk_slices : 1;
         dp_tiles = mode ? a.sk_tile_begin : tiles;
         rest = tiles - dp_tiles;
+        w = mode == 1 ? a.sk_w : 0;
         tail_unit = (mode && cluster < rest * slices) ? cluster : -1;
+        rem_e = (w > 0 && cluster >= rest * slices && cluster < rest * slices + a.sk_extra)
+                    ? cluster - rest * slices : -1;
+        rem_j = 0;
+        ncl = nclusters;
         t = cluster;
         step = nclusters;
     }
@@ -173,15 +199,29 @@ struct UnitIter {
             t += step;
             return true;
         }
-        if (tail_unit < 0) return false;
+        if (tail_unit < 0) {
+            // remainder units of an extra cluster: tiles rem_e, rem_e + E, ...
+            if (rem_e < 0) return false;
+            const int i = rem_e + rem_j * args->sk_extra;
+            if (i >= rest) return false;
+            u = Unit{dp_tiles + i, slices * w, kb, 0, BN, slices, remainder_slot(*args, rest, ncl, i)};
+            ++rem_j;
+            return true;
+        }
         const int s = tail_unit / rest;
         u.tile = dp_tiles + tail_unit % rest;
         u.slice = s;
+        u.slot = tail_unit;
         if (mode == 2) {  // N-split: half s of the tile's columns, full K
             u.k0 = 0;
             u.k1 = kb;
             u.width = BN / 2;
             u.n_off = s * (BN / 2);
+        } else if (w > 0) {  // K-slice s of a tail with a remainder slice
+            u.k0 = s * w;
+            u.k1 = (s + 1) * w;
+            u.n_off = 0;
+            u.width = BN;
         } else {          // K-slice s
             u.k0 = kb * s / slices;
             u.k1 = kb * (s + 1) / slices;
@@ -411,9 +451,42 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         UnitIter<BN> units(args, cluster, nclusters);
         Unit u;
         const int kb = args.k_blocks;
-        float* my_ws = args.workspace + static_cast<long>(cluster * kCtaGroup + pair_rank) * S::WS_FLOATS;
         uint32_t epi_chunk = 0;  // staged C chunks so far (alternating buffers)
-        while (units.next(u)) {
+        // TMEM -> RF -> SMEM for nch 32-column chunks into slot(c) (thread `row`
+        // writes bank row % 32: conflict-free), TMEM loads double-buffered; after
+        // each chunk pair one proxy fence + barrier, then one thread issues
+        // store(c), store(c+1) and commits them as a bulk group.
+        auto drain_pairs = [&](uint32_t tb, int nch, auto slot, auto store) {
+            uint32_t r0[32], r1[32];
+            tmem_ld_32x32b_x32(tb, r0);
+#pragma unroll 1
+            for (int c = 0; c < nch; c += 2) {
+                tmem_ld_wait();
+                tmem_ld_32x32b_x32(tb + (c + 1) * 32, r1);
+                float* d0 = slot(c) + row;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) d0[j * S::BM] = __uint_as_float(r0[j]);
+                tmem_ld_wait();
+                if (c + 2 < nch) tmem_ld_32x32b_x32(tb + (c + 2) * 32, r0);
+                float* d1 = slot(c + 1) + row;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) d1[j * S::BM] = __uint_as_float(r1[j]);
+                fence_proxy_async();
+                epilogue_bar();
+                if (q == 0 && lane == 0) {
+                    store(c);
+                    store(c + 1);
+                    bulk_commit_group();
+                }
+            }
+        };
+        // one unit of look-ahead: the cluster's last unit drains through the idle
+        // operand ring (no buffer reuse, one fence/barrier per chunk pair)
+        Unit nxt;
+        bool have = units.next(u);
+        while (have) {
+            const bool have_next = units.next(nxt);
+            const bool last_unit = !have_next;
             int tm, tn;
             tile_coords(args, u.tile, tm, tn);
             const int buf = it & 1;
@@ -436,7 +509,17 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     }
                     __syncwarp();
                 };
-                if (u.k0 == 0 && u.k1 == kb && args.c_tma) {
+                if (u.k0 == 0 && u.k1 == kb && args.c_tma && last_unit && args.ring_drain) {
+                    // the cluster's last unit: stage all chunks in the idle ring, TMA
+                    // store them pairwise; TMEM loads double-buffered
+                    const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
+                    float* stage0 = reinterpret_cast<float*>(ring);
+                    drain_pairs(tbase, u.width / 32, [&](int c) { return stage0 + c * (32 * S::BM); },
+                                [&](int c) {
+                                    tma_store_2d(&tmC, stage0 + c * (32 * S::BM), m_cta, tn * BN + u.n_off + c * 32);
+                                });
+                    release_tmem();
+                } else if (u.k0 == 0 && u.k1 == kb && args.c_tma) {
                     // whole K range, f32 col-major C: TMEM -> RF -> SMEM chunk -> TMA store.
                     // Column j of a chunk is 128 contiguous rows (512 B): thread `row`
                     // writes bank row % 32, conflict-free; one thread stores the chunk.
@@ -474,60 +557,96 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     }
                     release_tmem();
                 } else {
-                    // K-slice tail unit (the cluster's last unit: its ring is idle).
-                    // Symmetric fixup: slice s owns 32-column chunks [c_lo, c_hi);
-                    // it keeps those in smem, publishes every other chunk in its
-                    // workspace slot, then sums its own range over all slices in
-                    // slice (= K) order and stores it: deterministic, and the S
-                    // slices' fixups run in parallel.
+                    // K-slice tail unit. Symmetric fixup: main slice s owns 32-column
+                    // chunks [c_lo, c_hi) and keeps those in smem (a main slice is the
+                    // cluster's last unit: its operand ring is idle); every other chunk
+                    // is published in its workspace slot. A remainder slice owns no
+                    // columns and publishes all of them (its ring stays in use by the
+                    // next remainder unit). Each owner then sums its range over all
+                    // sources in K order (slices 0..S-1, then the remainder) and
+                    // stores it: deterministic, and the S fixups run in parallel.
                     const int nslc = args.sk_slices, s = u.slice;
+                    const bool remainder = s == nslc;
+                    const int nsrc = nslc + (args.sk_w > 0 ? 1 : 0);
                     const int rest = args.tiles_m * args.tiles_n - args.sk_tile_begin;
-                    const int tile_idx = cluster % rest;
+                    const int tile_idx = u.tile - args.sk_tile_begin;
                     constexpr int NCH = BN / 32;
-                    const int c_lo = NCH * s / nslc, c_hi = NCH * (s + 1) / nslc, nown = c_hi - c_lo;
+                    const int c_lo = remainder ? 0 : NCH * s / nslc;
+                    const int c_hi = remainder ? 0 : NCH * (s + 1) / nslc;
+                    const int nown = c_hi - c_lo;
                     constexpr uint32_t kChunkFloats = 32 * S::BM;
-                    float* own = reinterpret_cast<float*>(ring);         // [nown][32][128]
-                    float* peer = own + nown * kChunkFloats;              // [slices][nown][32][128]
+                    constexpr uint32_t kChunkBytes = kChunkFloats * 4;
+                    // main slice: the ring holds [own chunks][published chunks], the
+                    // latter reused for the peers' partials once they are stored
+                    float* own = reinterpret_cast<float*>(ring);  // [nown][32][128]
+                    float* peer = own + nown * kChunkFloats;       // [nsrc-1][nown][32][128]
+                    float* slot_ws = args.workspace + static_cast<long>(u.slot * kCtaGroup + pair_rank) * S::WS_FLOATS;
+                    // publish: every chunk that is not mine goes to the workspace slot
+                    // as one 16 KB bulk copy out of shared memory
+                    if (!remainder) {
+                        auto slot = [&](int c) {
+                            const bool mine = c >= c_lo && c < c_hi;
+                            return mine ? own + (c - c_lo) * kChunkFloats
+                                        : peer + (c < c_lo ? c : c - nown) * kChunkFloats;
+                        };
+                        drain_pairs(tbase, NCH, slot, [&](int c) {
+                            if (c < c_lo || c >= c_hi)
+                                bulk_copy_s2g(slot_ws + c * kChunkFloats, slot(c), kChunkBytes);
+                        });
+                    } else {
+                        // the ring is busy with the next unit: double-buffered epi staging
 #pragma unroll 1
-                    for (int c = 0; c < NCH; ++c) {
-                        uint32_t r[32];
-                        tmem_ld_32x32b_x32(tbase + c * 32, r);
-                        tmem_ld_wait();
-                        float* dst = (c >= c_lo && c < c_hi) ? own + (c - c_lo) * kChunkFloats + row
-                                                             : my_ws + c * kChunkFloats + row;
+                        for (int c = 0; c < NCH; ++c) {
+                            uint32_t r[32];
+                            tmem_ld_32x32b_x32(tbase + c * 32, r);
+                            float* stage = epi + (epi_chunk++ & 1) * kChunkFloats;
+                            if (q == 0 && lane == 0) bulk_wait_group_read<1>();
+                            epilogue_bar();
+                            tmem_ld_wait();
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) dst[j * S::BM] = __uint_as_float(r[j]);
+                            for (int j = 0; j < 32; ++j) stage[j * S::BM + row] = __uint_as_float(r[j]);
+                            fence_proxy_async();
+                            epilogue_bar();
+                            if (q == 0 && lane == 0) {
+                                bulk_copy_s2g(slot_ws + c * kChunkFloats, stage, kChunkBytes);
+                                bulk_commit_group();
+                            }
+                        }
                     }
                     release_tmem();
-                    __threadfence();
-                    epilogue_bar();  // all rows of my partial are out
                     if (q == 0 && lane == 0) {
-                        st_release_gpu(args.flags + (cluster * kCtaGroup + pair_rank), args.epoch);
+                        trace_stamp(args, it - 1, 6);
+                        bulk_wait_group<0>();        // my partial chunks are in global memory
+                        fence_proxy_async_global();  // async-proxy writes before the release
+                        trace_stamp(args, it - 1, 4);
+                        st_release_gpu(args.flags + (u.slot * kCtaGroup + pair_rank), args.epoch);
                         if (nown > 0) {
-                            mbar_arrive_expect_tx(&stage_bar[0], (nslc - 1) * nown * kChunkFloats * 4);
-                            for (int j = 0; j < nslc; ++j) {
+                            mbar_arrive_expect_tx(&stage_bar[0], (nsrc - 1) * nown * kChunkBytes);
+                            for (int j = 0; j < nsrc; ++j) {
                                 if (j == s) continue;
-                                const int pc = tile_idx + j * rest;  // cluster of slice j
-                                while (ld_acquire_gpu(args.flags + (pc * kCtaGroup + pair_rank)) < args.epoch)
+                                const int ps = j < nslc ? tile_idx + j * rest  // slot of source j
+                                                        : remainder_slot(args, rest, nclusters, tile_idx);
+                                while (ld_acquire_gpu(args.flags + (ps * kCtaGroup + pair_rank)) < args.epoch)
                                     __nanosleep(32);
-                                fence_proxy_async();
-                                bulk_copy_g2s(peer + j * nown * kChunkFloats,
+                                fence_proxy_async_global();
+                                bulk_copy_g2s(peer + (j < s ? j : j - 1) * nown * kChunkFloats,
                                               args.workspace +
-                                                  static_cast<long>(pc * kCtaGroup + pair_rank) * S::WS_FLOATS +
+                                                  static_cast<long>(ps * kCtaGroup + pair_rank) * S::WS_FLOATS +
                                                   static_cast<long>(c_lo) * kChunkFloats,
-                                              nown * kChunkFloats * 4, &stage_bar[0]);
+                                              nown * kChunkBytes, &stage_bar[0]);
                             }
                         }
                     }
                     __syncwarp();
                     if (nown > 0) {
                         mbar_wait(&stage_bar[0], 0);
+                        if (q == 0 && lane == 0) trace_stamp(args, it - 1, 5);
 #pragma unroll 1
                         for (int c = c_lo; c < c_hi; ++c) {
                             float v[32];
 #pragma unroll 1
-                            for (int j = 0; j < nslc; ++j) {
-                                const float* src = (j == s ? own : peer + j * nown * kChunkFloats) +
+                            for (int j = 0; j < nsrc; ++j) {
+                                const float* src = (j == s ? own : peer + (j < s ? j : j - 1) * nown * kChunkFloats) +
                                                    (c - c_lo) * kChunkFloats + row;
                                 if (j == 0) {
 #pragma unroll
@@ -537,7 +656,23 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                                     for (int x = 0; x < 32; ++x) v[x] += src[x * S::BM];
                                 }
                             }
-                            store_row32_any(args, m, tn * BN + c * 32, v);
+                            if (args.c_tma) {  // sum in place; TMA-stored below
+                                float* dst = own + (c - c_lo) * kChunkFloats + row;
+#pragma unroll
+                                for (int x = 0; x < 32; ++x) dst[x * S::BM] = v[x];
+                            } else {
+                                store_row32_any(args, m, tn * BN + c * 32, v);
+                            }
+                        }
+                        if (args.c_tma) {
+                            fence_proxy_async();
+                            epilogue_bar();
+                            if (q == 0 && lane == 0) {
+                                const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
+                                for (int c = c_lo; c < c_hi; ++c)
+                                    tma_store_2d(&tmC, own + (c - c_lo) * kChunkFloats, m_cta, tn * BN + c * 32);
+                                bulk_commit_group();
+                            }
                         }
                     }
                 }
@@ -602,6 +737,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 __syncwarp();
                 if (q == 0 && lane == 0) trace_stamp(args, it - 1, 3);
             }
+            u = nxt;
+            have = have_next;
         }
         if (q == 0 && lane == 0) bulk_wait_group<0>();  // TMA stores of C complete
         __syncwarp();

@@ -38,6 +38,7 @@ struct TcGemmProblem {
     int max_ctas = 0;                // 0 = persistent over all SMs
     int streamk = -1;                // -1 auto, 0 data-parallel, 1 K-slice tail, 2 N-split tail
     int force_slices = 0;            // >1: K-slice every tile into this many slices (.splitk on pairs)
+    int remainder = 1;               // K-slice tails may add a remainder slice on idle clusters
     // stream-K partial workspace; null = a library-owned pool. Launches that
     // share a workspace must be ordered on one stream.
     TcWorkspace* workspace = nullptr;
@@ -55,6 +56,7 @@ struct TcWorkspace {
 
 struct TcLaunchInfo {
     int ctas = 0, clusters = 0, streamk = 0;
+    int remainder = 0;  // K-slice tail with a remainder slice
 };
 TcLaunchInfo tc_gemm_last_launch();
 

@@ -15,6 +15,10 @@ def main(path):
         elif cur is not None:
             vals = [int(x) for x in line.split()]
             cur["rows"].append(tuple(vals[:6]))
+            if len(vals) >= 10 and vals[8]:  # tail fixup: published, peers staged, drained
+                cur.setdefault("fix", []).append((vals[4], vals[8], vals[9], vals[5]))
+                if len(vals) >= 11 and vals[10]:
+                    cur.setdefault("drain", []).append((vals[10] - vals[4], vals[8] - vals[10]))
             if len(vals) >= 8 and vals[6] and vals[7] and vals[3] > vals[2]:
                 cur.setdefault("mhz", []).append((vals[7] - vals[6]) / (vals[3] - vals[2]) * 1e3)
     last = launches[-1]
@@ -40,6 +44,21 @@ def main(path):
             print(f"unit {i}: starts {min(st) / 1e3:6.1f}..{max(st) / 1e3:6.1f} us  producer->MMA done median "
                   f"{statistics.median(mm) / 1e3:6.2f} us  epilogue median {statistics.median(ep) / 1e3 if ep else 0:6.2f} us"
                   f" max {max(ep) / 1e3 if ep else 0:6.2f}  (n={len(mm)})")
+
+
+    fix = last.get("fix")
+    if fix:
+        pub = [(p - r) / 1e3 for r, p, _, _ in fix]
+        stg = [(g - p) / 1e3 for _, p, g, _ in fix if g]
+        fin = [(d - g) / 1e3 for _, _, g, d in fix if g and d]
+        med = lambda x: statistics.median(x) if x else 0.0
+        print(f"tail fixup (median / max us): acc ready->partial published {med(pub):.2f} / {max(pub):.2f}  "
+              f"published->peers staged {med(stg):.2f} / {max(stg) if stg else 0:.2f}  "
+              f"staged->stored {med(fin):.2f} / {max(fin) if fin else 0:.2f}  (n={len(fix)}, owners={len(stg)})")
+        dr = last.get("drain")
+        if dr:
+            print(f"  of which TMEM->SMEM drain {med([d[0] / 1e3 for d in dr]):.2f} us, "
+                  f"bulk stores complete {med([d[1] / 1e3 for d in dr]):.2f} us (medians)")
 
 
 if __name__ == "__main__":
