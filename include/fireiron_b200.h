@@ -107,6 +107,24 @@ int64_t fi_script_validate(const char* script_utf8, int64_t m, int64_t n, int64_
                            int64_t cap);
 int64_t fi_script_elaborate(const char* script_utf8, int with_subs, char* buf, int64_t cap);
 int64_t fi_script_print(const char* script_utf8, char* buf, int64_t cap);
+/* CPU check of the asynchronous protocol of the launch a tcgen05 strategy
+ * lowers to (include/fireiron/async_check.hpp; the B200 analogue of the
+ * reference's race / ownership checks, proj/include/anvil/sim.hpp:63-104,
+ * 546-561). Writes the report text (first line "async protocol check: ok" or
+ * "... VIOLATIONS"); returns its length or -status. opts may be NULL. */
+typedef struct fi_async_check_options {
+    int32_t num_sms;             /* SMs of the modelled device (0 = 148)          */
+    int32_t max_active_clusters; /* occupancy cap (0 = num_sms / cluster size)    */
+    int32_t streamk;             /* -1 auto, 0 data-parallel, 1 K-slice, 2 N-split */
+    int32_t remainder;           /* remainder slices allowed (1)                  */
+    int32_t c_tma;               /* -1 as the launcher decides, 0 / 1 force       */
+    int32_t ring_drain;          /* last unit staged in the operand ring (1)      */
+    int32_t mutation;            /* fault injection for self-tests (0 = none)     */
+    int32_t reserved;
+} fi_async_check_options;
+int64_t fi_script_check_async(const char* script_utf8, int64_t m, int64_t n, int64_t k,
+                              const fi_async_check_options* opts, char* buf, int64_t cap);
+
 /* lower + emit the sm_100a CUDA text without compiling it (no GPU needed). */
 int64_t fi_script_codegen(const char* script_utf8, int64_t m, int64_t n, int64_t k, char* buf,
                           int64_t cap);

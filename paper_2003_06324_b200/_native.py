@@ -61,6 +61,12 @@ class PlanInfo(C.Structure):
                 ("remainder", C.c_int32), ("entry_name", C.c_char * 128)]
 
 
+class AsyncCheckOptions(C.Structure):
+    _fields_ = [("num_sms", C.c_int32), ("max_active_clusters", C.c_int32), ("streamk", C.c_int32),
+                ("remainder", C.c_int32), ("c_tma", C.c_int32), ("ring_drain", C.c_int32),
+                ("mutation", C.c_int32), ("reserved", C.c_int32)]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -85,6 +91,7 @@ def _load() -> C.CDLL:
         "fi_script_elaborate": ([C.c_char_p, C.c_int, C.c_char_p, i64], i64),
         "fi_script_print": ([C.c_char_p, C.c_char_p, i64], i64),
         "fi_script_codegen": ([C.c_char_p, i64, i64, i64, C.c_char_p, i64], i64),
+        "fi_script_check_async": ([C.c_char_p, i64, i64, i64, C.POINTER(AsyncCheckOptions), C.c_char_p, i64], i64),
     }
     for name, (args, res) in list(sigs.items()) + list(optional.items()):
         if not hasattr(lib, name):

@@ -61,6 +61,47 @@ def plan_summary(script: str, m: int = 0, n: int = 0, k: int = 0) -> str:
     return _text(N.lib.fi_script_plan, _enc(script), m, n, k)
 
 
+MUTATIONS = {"none": 0, "skip_empty_wait": 1, "ring_drain_every_unit": 2, "flag_before_bulk_wait": 3,
+             "skip_tmem_empty_wait": 4, "remainder_slot_collision": 5, "unpacked_peer_staging": 6}
+
+
+class AsyncReport:
+    """Result of check_async: counts plus the report text."""
+
+    def __init__(self, text: str):
+        import re
+        self.text = text
+        self.ok = text.startswith("async protocol check: ok")
+        nums = dict(re.findall(r"(events|races|capacity|coverage|deadlocks) (\d+)", text))
+        self.events = int(nums.get("events", 0))
+        self.races = int(nums.get("races", 0))
+        self.capacity_errors = int(nums.get("capacity", 0))
+        self.coverage_errors = int(nums.get("coverage", 0))
+        self.deadlocks = int(nums.get("deadlocks", 0))
+        m = re.search(r"schedule: (\d+) clusters x (\d+) CTAs, (\d+) tiles, (\d+) units, mode (\d+), "
+                      r"slices (\d+)( \+ remainder)?, split-k (\d+), stages (\d+)", text)
+        if m:
+            self.clusters, self.cluster_size, self.tiles, self.units, self.mode, self.slices = \
+                (int(x) for x in m.groups()[:6])
+            self.remainder = m.group(7) is not None
+            self.split_k, self.stages = int(m.group(8)), int(m.group(9))
+
+    def __repr__(self):
+        return self.text
+
+
+def check_async(script: str, m: int = 0, n: int = 0, k: int = 0, *, num_sms: int = 148,
+                max_active_clusters: int = 0, streamk: int = -1, remainder: int = 1, c_tma: int = -1,
+                ring_drain: int = 1, mutation: str = "none") -> AsyncReport:
+    """CPU check of the asynchronous protocol (mbarrier phases, TMA, tcgen05
+    commits, TMEM hand-off, bulk copies, epoch flags) of the launch a tcgen05
+    strategy lowers to: races, capacity, coverage, deadlock
+    (include/fireiron/async_check.hpp). No GPU needed."""
+    o = N.AsyncCheckOptions(num_sms, max_active_clusters, streamk, remainder, c_tma, ring_drain,
+                            MUTATIONS[mutation], 0)
+    return AsyncReport(_text(N.lib.fi_script_check_async, _enc(script), m, n, k, C.byref(o)))
+
+
 def _np_elem(code: int):
     return {N.FI_F32: np.float32, N.FI_F16: np.float16}.get(code)
 

@@ -5,6 +5,7 @@
 #include <memory>
 
 #include "../../../include/fireiron_b200.h"
+#include "fireiron/async_check.hpp"
 #include "fireiron/backend.hpp"
 #include "status.hpp"
 
@@ -164,6 +165,25 @@ int64_t fi_script_codegen(const char* script_utf8, int64_t m, int64_t n, int64_t
         ParsedScript ps = parse_script(script_utf8 ? script_utf8 : "");
         apply_size_overrides(ps, m, n, k);
         return generate(ps.root, ps.tree, ps.micro_kernels).source;
+    });
+}
+
+int64_t fi_script_check_async(const char* script_utf8, int64_t m, int64_t n, int64_t k,
+                              const fi_async_check_options* opts, char* buf, int64_t cap) {
+    return text_call(buf, cap, [&] {
+        ParsedScript ps = parse_script(script_utf8 ? script_utf8 : "");
+        apply_size_overrides(ps, m, n, k);
+        AsyncCheckOptions o;
+        if (opts) {
+            if (opts->num_sms > 0) o.num_sms = opts->num_sms;
+            o.max_active_clusters = opts->max_active_clusters;
+            o.streamk = opts->streamk;
+            o.remainder = opts->remainder;
+            o.c_tma = opts->c_tma;
+            o.ring_drain = opts->ring_drain;
+            o.mutation = opts->mutation;
+        }
+        return check_async(ps.root, ps.tree, o, ps.micro_kernels).to_string();
     });
 }
 

@@ -167,79 +167,24 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         max_active = n;
     }
     if (clusters > max_active) clusters = max_active;
-    // Tail split: whole waves data-parallel; the R leftover tiles of the partial
-    // last wave are cut into S K-slices so the idle clusters share them.
-    // S <= P/R (one unit per cluster), slices of >= 8 K-blocks, S <= 6 (the
-    // fixup stages S-1 partial chunks, double-buffered, in the operand ring).
     const int kb = args.k_blocks;
-    const int dp_clusters = clusters < tiles ? clusters : tiles;
-    const int full_waves = tiles / clusters;
-    const int rest = tiles - full_waves * clusters;
-    int slices = rest > 0 ? clusters / rest : 1;
-    if (slices > kb / 8) slices = kb / 8;
-    if (slices > 6) slices = 6;
-    // N-split of the partial last wave: two half-width units per leftover tile
-    const bool half_ok = BN >= 128 && (!cfg.b_mn_major || (BN / 2 / kCtaGroup) % 64 == 0);
-    const bool nsplit_ok = half_ok && rest > 0 && rest * 2 <= clusters;
-    int mode = 0;  // 0 data-parallel, 1 K-slice tail, 2 N-split tail
-    if (kSplitK == 1) {
-        // auto: K-slices when each slice still has >= 24 K-blocks to amortise
-        // the (parallel, ~5 us) fixup; otherwise N-split halves; else plain
-        // (measured at 4096^3 / 1024^2x32768 / 4096^2x1024, profiles/round1/)
-        if (p.streamk < 0)
-            mode = (slices >= 2 && kb / slices >= 24) ? 1 : (full_waves >= 1 && nsplit_ok) ? 2 : 0;
-        else if (p.streamk == 1) mode = slices >= 2 ? 1 : 0;
-        else if (p.streamk == 2) mode = nsplit_ok ? 2 : 0;
-    }
-    if (mode == 2) slices = 2;
-    // explicit split-K of every tile (a .splitk strategy on CTA pairs): all
-    // tiles are K-sliced across clusters, partials reduced in shared memory
-    int sk_begin = full_waves * clusters;
-    if (kSplitK == 1 && p.force_slices > 1) {
-        if (tiles * p.force_slices > clusters) return kTcErrShape;
-        mode = 1;
-        slices = p.force_slices;
-        sk_begin = 0;
-    }
-    // Remainder slice: with E = clusters - R*S extra clusters, main slices
-    // get W = ceil(q*kb / (S*q + 1)) K-blocks and the remainder kb - S*W runs
-    // on the extra clusters, q = ceil(R/E) remainders each, so every cluster
-    // has ~q*kb/(S*q+1) blocks instead of kb/S (C3: 114 vs 128). Only when the
-    // remainder units stay long enough (>= 24 blocks) to hide their own
-    // epilogue and the owners' staging of S+1 sources fits in the ring.
-    int sk_w = 0, sk_extra = 0, sk_q = 0;
-    if (mode == 1 && p.remainder != 0) {
-        const int rest_tiles = tiles - sk_begin;
-        const int extra = clusters - rest_tiles * slices;
-        const int e = extra < rest_tiles ? extra : rest_tiles;
-        if (e > 0) {
-            const int q = (rest_tiles + e - 1) / e;
-            const int w = (q * kb + slices * q) / (slices * q + 1);
-            const int rk = kb - slices * w;
-            constexpr int NCH = BN / 32;
-            const int nown = (NCH + slices - 1) / slices;
-            const bool fits = (slices + 1) * nown * 32 * S::BM * 4 <= S::RING_BYTES;
-            if (fits && rk >= 24 && q * rk <= w && w * 100 <= (kb / slices) * 97) {
-                sk_w = w;
-                sk_extra = e;
-                sk_q = q;
-            }
-        }
-    }
+    const SchedulePlan plan = plan_schedule<kCtaGroup, BN, kSplitK>(
+        tiles, kb, clusters, cfg.b_mn_major != 0, p.streamk, p.force_slices, p.remainder);
+    if (plan.status != 0) return kTcErrShape;
+    const int mode = plan.mode;
     const bool sk = mode != 0;
     if (dry_run) {
-        const int c = sk ? clusters : dp_clusters;
-        g_last = TcLaunchInfo{c * kCluster, c, mode, sk_w > 0 ? 1 : 0};
+        g_last = TcLaunchInfo{plan.clusters * kCluster, plan.clusters, mode, plan.sk_w > 0 ? 1 : 0};
         return kTcOk;
     }
     if (sk) {
-        args.sk_tile_begin = sk_begin;
-        args.sk_slices = slices;
-        args.sk_w = sk_w;
-        args.sk_extra = sk_extra;
-        args.sk_q = sk_q;
+        args.sk_tile_begin = plan.sk_begin;
+        args.sk_slices = plan.slices;
+        args.sk_w = plan.sk_w;
+        args.sk_extra = plan.sk_extra;
+        args.sk_q = plan.sk_q;
         TcWorkspace* ws = p.workspace ? p.workspace : shared_workspace();
-        const size_t slots = static_cast<size_t>(clusters) + (sk_q > 1 ? static_cast<size_t>(sk_extra) * (sk_q - 1) : 0);
+        const size_t slots = static_cast<size_t>(plan.slots);
         const size_t need_p = slots * kCtaGroup * S::WS_FLOATS;
         const size_t need_f = slots * kCtaGroup;
         if (ws->partial_floats < need_p) {
@@ -260,12 +205,10 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         args.workspace = ws->partials;
         args.flags = ws->flags;
         args.epoch = ++ws->epoch;
-    } else {
-        clusters = dp_clusters;
     }
-    if (clusters < 1) clusters = 1;
+    clusters = plan.clusters;
     lc.gridDim = dim3(clusters * kCluster, 1, 1);
-    g_last = TcLaunchInfo{clusters * kCluster, clusters, sk ? 1 : 0, sk_w > 0 ? 1 : 0};
+    g_last = TcLaunchInfo{clusters * kCluster, clusters, mode, plan.sk_w > 0 ? 1 : 0};
     // debugging aid: FI_TC_TRACE=<file> records a per-unit timeline of this launch
     const char* trace_path = std::getenv("FI_TC_TRACE");
     static unsigned long long* trace_buf = nullptr;

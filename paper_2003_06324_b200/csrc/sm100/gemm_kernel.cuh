@@ -37,48 +37,9 @@
 #include <cuda_fp16.h>
 
 #include "ptx.cuh"
+#include "schedule.hpp"
 
 namespace fireiron::sm100 {
-
-enum class OutType : int { F32 = 0, F16 = 1, BF16 = 2 };
-
-struct GemmArgs {
-    void* C = nullptr;
-    long ldc = 0;               // elements
-    int M = 0, N = 0, K = 0;
-    int tiles_m = 0, tiles_n = 0;
-    int k_blocks = 0;           // 64-wide K blocks per tile (per split-K rank)
-    int ab_format = 0;          // 0 = f16, 1 = bf16 (UMMA a/b format field)
-    int a_mn_major = 0;         // A stored M-contiguous (col-major M x K)
-    int b_mn_major = 0;         // B stored N-contiguous (row-major K x N)
-    int c_row_major = 0;
-    int out_type = 0;           // OutType
-    int group_m = 8;            // raster band (tile rows) for the default order
-    int stages = 0;             // pipeline depth actually used (0 = deepest that fits)
-    const int* tile_order = nullptr;  // optional permutation: Fireiron block-swizzle table
-    // stream-K
-    int streamk = 0;
-    int sk_tile_begin = 0;           // tiles before this index run data-parallel
-    int sk_slices = 1;               // K-slices per leftover tile
-    // remainder slices (K-slice tail only): main slice s covers K-blocks
-    // [s*sk_w, (s+1)*sk_w) and the remainder [sk_slices*sk_w, k_blocks) of
-    // leftover tile i runs on extra cluster rest*sk_slices + i % sk_extra as
-    // its (i / sk_extra)-th unit; sk_w = 0: even slices, no remainder
-    int sk_w = 0;
-    int sk_extra = 0;
-    int sk_q = 0;
-    int c_tma = 0;                   // f32 col-major C stored by TMA from smem staging
-    int ring_drain = 1;              // the cluster's last unit stages C in the idle operand ring
-    float* workspace = nullptr;     // [slots][kCtaGroup][BN][128] fp32 partials
-    unsigned* flags = nullptr;       // [slots][kCtaGroup] epoch of the published partial
-                                     // slots: one per cluster + sk_extra*(sk_q-1)
-    unsigned epoch = 0;              // this launch's epoch (> every earlier launch's)
-    // optional timeline (FI_TC_TRACE): [cta][unit < 16][16] %globaltimer stamps
-    // [0..7] and clock64 [8..15] of: producer first load, MMA last commit,
-    // epilogue accumulator ready, epilogue done, tail partial published, tail
-    // peers staged
-    unsigned long long* trace = nullptr;
-};
 
 __device__ __forceinline__ unsigned long long global_timer_ns() {
     unsigned long long t;
@@ -91,147 +52,6 @@ __device__ __forceinline__ void trace_stamp(const GemmArgs& a, int unit, int ev)
         a.trace[(blockIdx.x * 16 + unit) * 16 + 8 + ev] = clock64();  // SM clock: effective MHz
     }
 }
-
-template <int kCtaGroup, int BN, int kSplitK>
-struct GemmShape {
-    static constexpr int BM = 128;                 // rows per CTA (TMEM lanes)
-    static constexpr int BM_TILE = 128 * kCtaGroup;
-    static constexpr int BK = 64;                  // one 128B swizzle span of 16-bit
-    static constexpr int BN_LOCAL = BN / kCtaGroup;
-    static constexpr int A_BYTES = BM * BK * 2;
-    static constexpr int B_BYTES = BN_LOCAL * BK * 2;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    // split-K reduction scratch: the fp32 partial tile (rows padded by 16B)
-    // reuses the operand ring once the tile's main loop has drained it
-    static constexpr int RED_LD = BN + 4;
-    static constexpr int RED_BYTES = kSplitK > 1 ? BM * RED_LD * 4 : 0;
-    static constexpr int kStages = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-    static_assert(kStages >= 2, "pipeline needs at least two stages");
-    static constexpr int kAccBufs = 2;
-    static constexpr int TMEM_COLS_RAW = kAccBufs * BN;
-    static constexpr int TMEM_COLS = TMEM_COLS_RAW <= 32    ? 32
-                                     : TMEM_COLS_RAW <= 64  ? 64
-                                     : TMEM_COLS_RAW <= 128 ? 128
-                                     : TMEM_COLS_RAW <= 256 ? 256
-                                                            : 512;
-    static constexpr int RING_BYTES = kStages * STAGE_BYTES;
-    static constexpr int BAR_BYTES = 256;
-    static_assert(RED_BYTES <= RING_BYTES, "split-K scratch must fit in the operand ring");
-    // epilogue staging for TMA stores of C: two 32-column x 128-row fp32 chunks
-    static constexpr int EPI_CHUNK_BYTES = 32 * BM * 4;
-    static constexpr int EPI_BYTES = 2 * EPI_CHUNK_BYTES;
-    static constexpr int SMEM_BYTES = RING_BYTES + EPI_BYTES + BAR_BYTES + 1024;  // + align slack
-    static_assert(SMEM_BYTES <= 227 * 1024, "exceeds the sm_100a per-CTA shared memory");
-    static constexpr int kThreads = 256;
-    static constexpr int WS_FLOATS = BN * BM;     // one CTA's partial tile
-};
-
-// Tile id -> (tile row, tile col). With an explicit order table (the strategy's
-// Block .swizzle) the unit id maps RowMajor as in Fireiron: row = u % tiles_m.
-// Otherwise a grouped raster keeps a band of group_m A panels L2-resident while
-// sweeping N.
-__device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, int& tn) {
-    if (a.tile_order) {
-        const int u = a.tile_order[t];
-        tm = u % a.tiles_m;
-        tn = u / a.tiles_m;
-        return;
-    }
-    const int band = a.group_m * a.tiles_n;
-    const int g = t / band;
-    const int local = t - g * band;
-    int rows = a.tiles_m - g * a.group_m;
-    if (rows > a.group_m) rows = a.group_m;
-    tm = g * a.group_m + local % rows;
-    tn = local / rows;
-}
-
-// One work unit: K-blocks [k0, k1) of columns [n_off, n_off + width) of tile `tile`.
-struct Unit {
-    int tile, k0, k1;
-    int n_off, width;
-    int slice;  // K-slice index of a tail unit (sk_slices for a remainder)
-    int slot;   // workspace slot its partial is published in (tail units)
-};
-
-// Workspace slot of the remainder partial of leftover tile i.
-__device__ __forceinline__ int remainder_slot(const GemmArgs& a, int rest, int nclusters, int i) {
-    const int e = i % a.sk_extra, j = i / a.sk_extra;
-    return j == 0 ? rest * a.sk_slices + e : nclusters + e * (a.sk_q - 1) + j - 1;
-}
-
-// The unit sequence of one cluster. Tiles [0, D) run data-parallel (tile
-// cluster, cluster+P, ...: consecutive clusters work on neighbouring tiles and
-// advance through K in lockstep, so a wave's A/B panels are read once from
-// DRAM). The R = T - D leftover tiles (the partial last wave) are split into S
-// K-slices at fixed offsets: cluster c < R*S takes slice c / R of tile
-// D + c % R. Clusters in the same slice stay in K lockstep (L2 reuse again),
-// and slice 0 -- whose cluster also holds the K prefix -- owns the fixup.
-// With args.streamk == 2 the leftover tiles are instead split along N into two
-// half-width units (tcgen05 MMA with N = BN/2): no partials and no fixup.
-template <int BN>
-struct UnitIter {
-    int t, step, kb, dp_tiles, tail_unit;
-    int slices, rest, mode, w;
-    int rem_e, rem_j, ncl;
-    const GemmArgs* args;
-
-    __device__ UnitIter(const GemmArgs& a, int cluster, int nclusters) {
-        args = &a;
-        kb = a.k_blocks;
-        const int tiles = a.tiles_m * a.tiles_n;
-        mode = a.streamk;
-        slices = mode ? a.sk_slices : 1;
-        dp_tiles = mode ? a.sk_tile_begin : tiles;
-        rest = tiles - dp_tiles;
-        w = mode == 1 ? a.sk_w : 0;
-        tail_unit = (mode && cluster < rest * slices) ? cluster : -1;
-        rem_e = (w > 0 && cluster >= rest * slices && cluster < rest * slices + a.sk_extra)
-                    ? cluster - rest * slices : -1;
-        rem_j = 0;
-        ncl = nclusters;
-        t = cluster;
-        step = nclusters;
-    }
-    __device__ bool next(Unit& u) {
-        if (t < dp_tiles) {
-            u = Unit{t, 0, kb, 0, BN, 0};
-            t += step;
-            return true;
-        }
-        if (tail_unit < 0) {
-            // remainder units of an extra cluster: tiles rem_e, rem_e + E, ...
-            if (rem_e < 0) return false;
-            const int i = rem_e + rem_j * args->sk_extra;
-            if (i >= rest) return false;
-            u = Unit{dp_tiles + i, slices * w, kb, 0, BN, slices, remainder_slot(*args, rest, ncl, i)};
-            ++rem_j;
-            return true;
-        }
-        const int s = tail_unit / rest;
-        u.tile = dp_tiles + tail_unit % rest;
-        u.slice = s;
-        u.slot = tail_unit;
-        if (mode == 2) {  // N-split: half s of the tile's columns, full K
-            u.k0 = 0;
-            u.k1 = kb;
-            u.width = BN / 2;
-            u.n_off = s * (BN / 2);
-        } else if (w > 0) {  // K-slice s of a tail with a remainder slice
-            u.k0 = s * w;
-            u.k1 = (s + 1) * w;
-            u.n_off = 0;
-            u.width = BN;
-        } else {          // K-slice s
-            u.k0 = kb * s / slices;
-            u.k1 = kb * (s + 1) / slices;
-            u.n_off = 0;
-            u.width = BN;
-        }
-        tail_unit = -1;
-        return true;
-    }
-};
 
 template <typename T>
 __device__ __forceinline__ T cvt_out(float v);

@@ -16,6 +16,7 @@
 #include <sstream>
 #include <string>
 
+#include "fireiron/async_check.hpp"
 #include "fireiron/anvil.hpp"
 
 using namespace fireiron;
@@ -33,7 +34,7 @@ struct Args {
 
 [[noreturn]] void usage() {
     std::fprintf(stderr,
-                 "usage: fireiron {elaborate|codegen|simulate|verify} <script.fi> [--m M] [--n N] [--k K]\n"
+                 "usage: fireiron {elaborate|codegen|simulate|verify|check-async} <script.fi> [--m M] [--n N] [--k K]\n"
                  "       [--seed S] [--float] [--load-a F] [--load-b F] [--dump-c F] [--tolerance T]\n"
                  "       [--dump-trace] [--out F]\n");
     std::exit(2);
@@ -152,6 +153,12 @@ int main(int argc, char** argv) {
                 o << ks.source;
             }
             return 0;
+        }
+        if (a.cmd == "check-async") {  // CPU protocol check of the tcgen05 launch (no GPU)
+            ParsedScript s = load(a);
+            const AsyncReport r = check_async(s.root, s.tree, AsyncCheckOptions{}, s.micro_kernels);
+            std::cout << r.to_string();
+            return r.ok() ? 0 : 1;
         }
         if (a.cmd == "simulate" || a.cmd == "verify") {
             ParsedScript s = load(a);

@@ -1,0 +1,100 @@
+"""CPU checker of the tcgen05 launch protocol (include/fireiron/async_check.hpp,
+SURVEY.md 8(f) rank 4): every strategy the GPU tests and the bench run must
+replay race-free, within its shared-memory / TMEM / workspace allocations,
+storing each output chunk exactly once; every injected protocol fault must
+be reported -- the B200 counterpart of the reference's race and ownership
+checks (proj/include/anvil/sim.hpp:63-104, 546-561; tests/test_sim.cpp)."""
+import pytest
+
+
+@pytest.fixture(scope="module")
+def tc(fi):
+    return fi.strategies.tc_strategy
+
+
+CFGS = [dict(pair=True, tile_n=256), dict(pair=True, tile_n=128), dict(pair=False, tile_n=256),
+        dict(pair=False, tile_n=128), dict(pair=False, tile_n=64)]
+LAYOUTS = [("colmajor", "colmajor", "colmajor"), ("rowmajor", "colmajor", "colmajor"),
+           ("colmajor", "rowmajor", "rowmajor"), ("rowmajor", "rowmajor", "colmajor")]
+
+
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: f"pair{int(c['pair'])}_n{c['tile_n']}")
+@pytest.mark.parametrize("layouts", LAYOUTS, ids=lambda l: "".join(x[0] for x in l))
+@pytest.mark.parametrize("cout", ["f32", "f16"])
+def test_gpu_test_strategies_are_race_free(fi, tc, cfg, layouts, cout):
+    m, n, k = 512, 768 if cfg["tile_n"] != 256 else 512, 320
+    r = fi.check_async(tc(m, n, k, layouts=layouts, c=cout, **cfg))
+    assert r.ok, r.text
+
+
+@pytest.mark.parametrize("pair,tile_n,split", [(False, 128, 2), (False, 128, 4), (False, 256, 4),
+                                               (True, 256, 2), (True, 256, 4), (True, 128, 2)])
+@pytest.mark.parametrize("k", [4096, 16384])
+def test_splitk_lowerings_are_race_free(fi, tc, pair, tile_n, split, k):
+    # pairs: cross-cluster K slices (+ remainder at k=16384); 1-CTA: cluster DSMEM reduction
+    r = fi.check_async(tc(512, 512, k, pair=pair, tile_n=tile_n, split_k=split))
+    assert r.ok, r.text
+    assert r.split_k == split
+
+
+@pytest.mark.parametrize("mode", [-1, 0, 1, 2])
+@pytest.mark.parametrize("shape", [(4096, 4096, 4096), (4096, 4096, 1024), (2560, 2560, 10240), (768, 1024, 9600),
+                                   (4096, 4096, 32768), (8192, 8192, 2048)])
+def test_tail_schedules_are_race_free(fi, tc, mode, shape):
+    r = fi.check_async(tc(*shape), streamk=mode)
+    assert r.ok, r.text
+
+
+def test_bench_workload_schedules(fi, tc):
+    """The schedules the bench lines measure."""
+    c2 = fi.check_async(fi.strategies.c2_strategy())
+    assert c2.ok and c2.mode == 1 and c2.slices == 2 and not c2.remainder and c2.units == 222 + 68
+    c3 = fi.check_async(fi.strategies.c3_strategy())
+    assert c3.ok and c3.mode == 1 and c3.slices == 4 and c3.remainder and c3.clusters == 74
+    assert c3.units == 16 * 4 + 16  # 64 main slices + 16 remainders on 10 extra clusters
+    c5 = fi.check_async(fi.strategies.c5_strategy(2048, 2048, 16384))  # an 8-way shard chunk
+    assert c5.ok
+
+
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (2048, 2048, 2048), (4096, 256, 4096), (512, 8192, 8192)])
+def test_sweep_strategies_are_race_free(fi, m, n, k):
+    for name, script in fi.strategies.sweep_strategies(m, n, k).items():
+        r = fi.check_async(script)
+        assert r.ok, (name, r.text)
+
+
+@pytest.mark.parametrize("stages", [2, 3, 4])
+def test_shallow_rings_are_race_free(fi, tc, stages):
+    r = fi.check_async(tc(1024, 1024, 2048, stages=stages))
+    assert r.ok and r.stages == stages, r.text
+
+
+def test_without_ring_drain_or_tma_store(fi, tc):
+    assert fi.check_async(tc(4096, 4096, 1024), ring_drain=0).ok
+    assert fi.check_async(tc(4096, 4096, 1024), c_tma=0).ok
+
+
+# ---------------------------------------------------------------- fault injection
+MUTANTS = [
+    ("ring_drain_every_unit", (4096, 4096, 1024), {}, "races"),           # C staged over in-flight TMA loads
+    ("flag_before_bulk_wait", (1024, 1024, 32768), dict(split_k=4), "races"),  # peers read unwritten partials
+    ("skip_tmem_empty_wait", (4096, 4096, 1024), {}, "races"),            # MMA overwrites an undrained accumulator
+    ("remainder_slot_collision", (1024, 1024, 32768), dict(split_k=4), "races"),
+    ("unpacked_peer_staging", (768, 1024, 9600), {}, "capacity_errors"),  # 6 slices: staging past the ring
+    ("skip_empty_wait", (1024, 1024, 4096), {}, "deadlocks"),             # parity runs ahead of the consumer
+]
+
+
+@pytest.mark.parametrize("mutation,shape,kw,field", MUTANTS, ids=[m[0] for m in MUTANTS])
+def test_injected_faults_are_reported(fi, tc, mutation, shape, kw, field):
+    clean = fi.check_async(tc(*shape, **kw))
+    assert clean.ok, clean.text
+    bad = fi.check_async(tc(*shape, **kw), mutation=mutation)
+    assert not bad.ok
+    assert getattr(bad, field) > 0, bad.text
+
+
+def test_non_tensor_core_tree_is_rejected(fi):
+    from paper_2003_06324_b200 import FiError
+    with pytest.raises(FiError):
+        fi.check_async(fi.strategies.listing2(128, 128, 32))

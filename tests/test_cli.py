@@ -67,3 +67,13 @@ def test_cli_verify_tensor_core_strategy(tmp_path):
     s.write_text(fi.strategies.tc_strategy(512, 512, 256))
     r = run("verify", str(s), "--seed", "3")
     assert r.returncode == 0 and "backend=tcgen05" in r.stdout and r.stdout.startswith("PASS max_error=0 ")
+
+
+def test_cli_check_async(tmp_path, fi):  # CPU protocol check of the tcgen05 launch
+    f = tmp_path / "c3.fi"
+    f.write_text(fi.strategies.c3_strategy())
+    r = run("check-async", str(f))
+    assert r.returncode == 0 and r.stdout.startswith("async protocol check: ok")
+    assert "slices 4 + remainder" in r.stdout
+    r = run("check-async", L2)  # FMA-leaf tree: no tcgen05 lowering
+    assert r.returncode == 1 and "InvalidTree" in r.stderr

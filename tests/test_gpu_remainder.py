@@ -16,6 +16,7 @@ CASES = [
     (512, 512, 16384, dict(pair=True, tile_n=256, split_k=4), True),    # q=1
     (2560, 2560, 10240, dict(pair=True, tile_n=256), True),             # 1 data-parallel wave + tail S=2, q=2
     (512, 512, 4096, dict(pair=True, tile_n=256, split_k=4), False),    # remainder too short: even slices
+    (768, 1024, 9600, dict(pair=True, tile_n=256), False),              # 12 tiles -> 6 even K slices (peer staging fills the ring)
 ]
 
 
