@@ -48,6 +48,8 @@ struct AsyncCheckOptions {
     int remainder = 1;            // as FI_REMAINDER
     int c_tma = -1;               // -1 as the launcher decides (f32 column-major C), 0/1 force
     int ring_drain = 1;           // as FI_TC_RING_DRAIN
+    int pull_d = -2;              // as FI_TC_PULL_D: -2 the launcher's default, -1 no pull fixup
+    int head = 1;                 // as FI_TC_HEAD: 2-slice pull tails run before the data-parallel tiles
     int mutation = kMutNone;
 };
 
@@ -63,7 +65,7 @@ struct AsyncReport {
     long events = 0;  // checked accesses
     long races = 0, capacity_errors = 0, coverage_errors = 0, deadlocks = 0;
     // the schedule that was checked
-    int clusters = 0, cluster_size = 1, mode = 0, slices = 1, remainder = 0, split_k = 1, stages = 0;
+    int clusters = 0, cluster_size = 1, mode = 0, slices = 1, remainder = 0, pull = 0, head = 0, split_k = 1, stages = 0;
     long units = 0, tiles = 0;
     std::vector<AsyncRecord> records;  // first 256
     bool ok() const { return races == 0 && capacity_errors == 0 && coverage_errors == 0 && deadlocks == 0; }

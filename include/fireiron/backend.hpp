@@ -96,7 +96,7 @@ struct PlanInfo {
     long launch_ctas = 0;
     int cluster = 1, stages = 0, tmem_cols = 0, cta_group = 1, tile_m = 0, tile_n = 0, split_k = 1;
     int streamk = 0;  // tcgen05 plans: 0 data-parallel, 1 K-sliced tail/split, 2 N-split tail
-    int remainder = 0;  // K-slice tail with a remainder slice on the idle clusters
+    int remainder = 0;  // K-slice tail: 1 remainder slices on the idle clusters, 2 two-slice pull fixup
     int splitk_global = 0;  // .splitk lowered to cross-cluster K slices (else DSMEM cluster)
     long shared_bytes = 0;
     double flops = 0.0;

@@ -67,7 +67,7 @@ typedef struct fi_plan_info {
     int64_t shared_bytes;         /* dynamic smem per CTA                       */
     double flops;                 /* 2*M*N*K (0 for Move)                       */
     int32_t streamk;              /* stream-K partitioning of (tile, K-block) work */
-    int32_t remainder;            /* K-slice tail adds a remainder slice on idle clusters */
+    int32_t remainder;            /* K-slice tail: 1 remainder slices on idle clusters, 2 pull fixup */
     char entry_name[128];
 } fi_plan_info;
 
@@ -120,7 +120,8 @@ typedef struct fi_async_check_options {
     int32_t c_tma;               /* -1 as the launcher decides, 0 / 1 force       */
     int32_t ring_drain;          /* last unit staged in the operand ring (1)      */
     int32_t mutation;            /* fault injection for self-tests (0 = none)     */
-    int32_t reserved;
+    int32_t pull_d;              /* 2-slice pull fixup: -2 launcher default, -1 off */
+    int32_t head;                /* pull-fixup tails before data-parallel tiles (1) */
 } fi_async_check_options;
 int64_t fi_script_check_async(const char* script_utf8, int64_t m, int64_t n, int64_t k,
                               const fi_async_check_options* opts, char* buf, int64_t cap);

@@ -79,12 +79,14 @@ class AsyncReport:
         self.coverage_errors = int(nums.get("coverage", 0))
         self.deadlocks = int(nums.get("deadlocks", 0))
         m = re.search(r"schedule: (\d+) clusters x (\d+) CTAs, (\d+) tiles, (\d+) units, mode (\d+), "
-                      r"slices (\d+)( \+ remainder)?, split-k (\d+), stages (\d+)", text)
+                      r"slices (\d+)( \+ remainder)?( \(pull fixup(, first)?\))?, split-k (\d+), stages (\d+)", text)
         if m:
             self.clusters, self.cluster_size, self.tiles, self.units, self.mode, self.slices = \
                 (int(x) for x in m.groups()[:6])
             self.remainder = m.group(7) is not None
-            self.split_k, self.stages = int(m.group(8)), int(m.group(9))
+            self.pull = m.group(8) is not None
+            self.head = m.group(9) is not None
+            self.split_k, self.stages = int(m.group(10)), int(m.group(11))
 
     def __repr__(self):
         return self.text
@@ -92,13 +94,13 @@ class AsyncReport:
 
 def check_async(script: str, m: int = 0, n: int = 0, k: int = 0, *, num_sms: int = 148,
                 max_active_clusters: int = 0, streamk: int = -1, remainder: int = 1, c_tma: int = -1,
-                ring_drain: int = 1, mutation: str = "none") -> AsyncReport:
+                ring_drain: int = 1, pull_d: int = -2, head: int = 1, mutation: str = "none") -> AsyncReport:
     """CPU check of the asynchronous protocol (mbarrier phases, TMA, tcgen05
     commits, TMEM hand-off, bulk copies, epoch flags) of the launch a tcgen05
     strategy lowers to: races, capacity, coverage, deadlock
     (include/fireiron/async_check.hpp). No GPU needed."""
     o = N.AsyncCheckOptions(num_sms, max_active_clusters, streamk, remainder, c_tma, ring_drain,
-                            MUTATIONS[mutation], 0)
+                            MUTATIONS[mutation], pull_d, head)
     return AsyncReport(_text(N.lib.fi_script_check_async, _enc(script), m, n, k, C.byref(o)))
 
 

@@ -37,7 +37,8 @@ std::string AsyncReport::to_string() const {
     std::ostringstream os;
     os << "async protocol check: " << (ok() ? "ok" : "VIOLATIONS") << "\n"
        << "  schedule: " << clusters << " clusters x " << cluster_size << " CTAs, " << tiles << " tiles, " << units
-       << " units, mode " << mode << ", slices " << slices << (remainder ? " + remainder" : "") << ", split-k "
+       << " units, mode " << mode << ", slices " << slices << (remainder ? " + remainder" : "")
+       << (pull ? (head ? " (pull fixup, first)" : " (pull fixup)") : "") << ", split-k "
        << split_k << ", stages " << stages << "\n"
        << "  events " << events << ", races " << races << ", capacity " << capacity_errors << ", coverage "
        << coverage_errors << ", deadlocks " << deadlocks << "\n";
@@ -137,7 +138,8 @@ public:
         for (auto& c : ctas_) {
             c.full.resize(kStages);
             c.empty.resize(kStages);
-            for (auto* b : {&c.tfull[0], &c.tfull[1], &c.tempty[0], &c.tempty[1], &c.rfull, &c.rempty, &c.stage})
+            for (auto* b : {&c.tfull[0], &c.tfull[1], &c.tempty[0], &c.tempty[1], &c.rfull, &c.rempty, &c.stage,
+                            &c.pstage[0], &c.pstage[1]})
                 init_bar(*b, 1);
             for (auto& b : c.full) init_bar(b, 1);
             for (auto& b : c.empty) init_bar(b, 1);
@@ -201,7 +203,7 @@ public:
 private:
     struct Cta {
         std::vector<Barrier> full, empty;
-        Barrier tfull[2], tempty[2], rfull, rempty, stage;
+        Barrier tfull[2], tempty[2], rfull, rempty, stage, pstage[2];
         std::deque<std::pair<Clock, Clock>> groups;  // committed bulk groups: (read clock, write clock)
         long committed = 0, waited_r = 0, waited_w = 0;
     };
@@ -501,6 +503,71 @@ private:
                         store_c(E, tile, ch_off + c);
                     }
                     release_tmem();
+                } else if (a_.sk_pull) {
+                    // 2-slice pull fixup
+                    const int rest = a_.tiles_m * a_.tiles_n - a_.sk_tile_begin;
+                    const int tile_idx = u.tile - a_.sk_tile_begin;
+                    if (u.slice == 1) {
+                        for (int c = 0; c < NCH; ++c) {
+                            tmem(E, cta, buf, c * 32, 32, false);
+                            if (a_.sk_head) {  // ring busy: double-buffered epi staging
+                                const long off = static_cast<long>(epi_chunk++ & 1) * kChunkBytes;
+                                wait_groups(cta, 1, false);
+                                smem(E, cta, kEpi, off, kChunkBytes, true);
+                                bulk_store(kEpi, off, [&](int bw) { workspace(bw, u.slot, c, 1, true); });
+                                commit_group(cta);
+                                continue;
+                            }
+                            smem(E, cta, kRing, static_cast<long>(c) * kChunkBytes, kChunkBytes, true);
+                            if (c & 1) {
+                                for (int x = c - 1; x <= c; ++x)
+                                    bulk_store(kRing, static_cast<long>(x) * kChunkBytes,
+                                               [&](int bw) { workspace(bw, u.slot, x, 1, true); });
+                                commit_group(cta);
+                            }
+                        }
+                        release_tmem();
+                        if (opt_.mutation != kMutFlagBeforeBulkWait) wait_groups(cta, 0, true);
+                        tick();
+                        Flag& f = flags_[static_cast<size_t>(u.slot)];
+                        f.value = a_.epoch;
+                        f.clock = ve;
+                        if (opt_.mutation == kMutFlagBeforeBulkWait) wait_groups(cta, 0, true);
+                    } else {
+                        const long ps = tile_idx + static_cast<long>(rest);
+                        Flag& pf = flags_[static_cast<size_t>(ps)];
+                        co_await WaitUntil{[&pf, this] { return pf.value >= a_.epoch; }};
+                        join(ve, pf.clock);
+                        wait_groups(cta, 0, false);  // bulk_wait_group_read<0>
+                        auto fetch = [&](int c) {    // bulk g2s of peer chunk c into epi[c & 1]
+                            Barrier& sb = C.pstage[c & 1];
+                            expect_tx(sb, kChunkBytes);
+                            tick();
+                            arrive(sb, ve);
+                            issue(G, E);
+                            workspace(G, ps, c, 1, false);
+                            smem(G, cta, kEpi, static_cast<long>(c & 1) * kChunkBytes, kChunkBytes, true);
+                            complete_tx(sb, kChunkBytes, vc_[static_cast<size_t>(G)]);
+                        };
+                        fetch(0);
+                        fetch(1);
+                        for (int c = 0; c < NCH; ++c) {
+                            tmem(E, cta, buf, c * 32, 32, false);
+                            Barrier& sb = C.pstage[c & 1];
+                            co_await wait(sb, static_cast<uint32_t>(c >> 1) & 1);
+                            acquire(E, sb, static_cast<uint32_t>(c >> 1) & 1);
+                            smem(E, cta, kEpi, static_cast<long>(c & 1) * kChunkBytes, kChunkBytes, false);
+                            if (c + 2 < NCH) fetch(c + 2);
+                            if (a_.c_tma && !a_.sk_head) {
+                                smem(E, cta, kRing, static_cast<long>(c) * kChunkBytes, kChunkBytes, true);
+                                bulk_store(kRing, static_cast<long>(c) * kChunkBytes, [&](int bw) { store_c(bw, tile, c); });
+                                commit_group(cta);
+                            } else {
+                                store_c(E, tile, c);
+                            }
+                        }
+                        release_tmem();
+                    }
                 } else {
                     // K-slice tail unit: symmetric fixup
                     const int nslc = a_.sk_slices, s = u.slice;
@@ -629,7 +696,8 @@ void run_checker(GemmArgs args, int sms, int force_slices, const AsyncCheckOptio
     if (o.max_active_clusters > 0 && o.max_active_clusters < clusters) clusters = o.max_active_clusters;
     const SchedulePlan plan = plan_schedule<kCtaGroup, BN, kSplitK>(tiles, args.k_blocks, clusters,
                                                                     args.b_mn_major != 0, o.streamk,
-                                                                    force_slices, o.remainder);
+                                                                    force_slices, o.remainder,
+                                                                    o.pull_d == -2 ? BN / 32 : o.pull_d, o.head);
     rep.tiles = tiles;
     rep.cluster_size = kCluster;
     rep.split_k = kSplitK > 1 ? kSplitK : (force_slices > 1 ? force_slices : 1);
@@ -646,12 +714,16 @@ void run_checker(GemmArgs args, int sms, int force_slices, const AsyncCheckOptio
         args.sk_w = plan.sk_w;
         args.sk_extra = plan.sk_extra;
         args.sk_q = plan.sk_q;
+        args.sk_pull = plan.sk_pull;
+        args.sk_head = plan.sk_head;
     }
     args.epoch = 1;
     rep.clusters = plan.clusters;
     rep.mode = plan.mode;
     rep.slices = plan.slices;
-    rep.remainder = plan.sk_w > 0 ? 1 : 0;
+    rep.remainder = plan.sk_w > 0 && !plan.sk_pull ? 1 : 0;
+    rep.pull = plan.sk_pull;
+    rep.head = plan.sk_head;
     for (int c = 0; c < plan.clusters; ++c) {
         UnitIter<BN> it(args, c, plan.clusters);
         Unit u;

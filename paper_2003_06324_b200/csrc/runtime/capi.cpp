@@ -182,6 +182,8 @@ int64_t fi_script_check_async(const char* script_utf8, int64_t m, int64_t n, int
             o.c_tma = opts->c_tma;
             o.ring_drain = opts->ring_drain;
             o.mutation = opts->mutation;
+            o.pull_d = opts->pull_d;
+            o.head = opts->head;
         }
         return check_async(ps.root, ps.tree, o, ps.micro_kernels).to_string();
     });

@@ -121,6 +121,16 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         return !(v && v[0] == '0');
     }();
     args.ring_drain = ring_drain_env ? 1 : 0;
+    static const int l2_hint_env = [] {
+        const char* v = std::getenv("FI_TC_L2HINT");
+        return v ? std::atoi(v) : 0;
+    }();
+    args.l2_hint = l2_hint_env;
+    static const int epi_sleep_env = [] {
+        const char* v = std::getenv("FI_TC_EPI_SLEEP");
+        return v ? std::atoi(v) : 256;
+    }();
+    args.epi_sleep_ns = static_cast<unsigned>(epi_sleep_env);
 
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
@@ -168,13 +178,22 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     }
     if (clusters > max_active) clusters = max_active;
     const int kb = args.k_blocks;
+    // FI_TC_PULL_D: publish time of the 2-slice pull fixup in K-blocks (-1 disables)
+    static const int pull_d_env = [] {
+        const char* v = std::getenv("FI_TC_PULL_D");
+        return v ? std::atoi(v) : BN / 32;
+    }();
+    static const int head_env = [] {
+        const char* v = std::getenv("FI_TC_HEAD");
+        return v ? std::atoi(v) : 1;
+    }();
     const SchedulePlan plan = plan_schedule<kCtaGroup, BN, kSplitK>(
-        tiles, kb, clusters, cfg.b_mn_major != 0, p.streamk, p.force_slices, p.remainder);
+        tiles, kb, clusters, cfg.b_mn_major != 0, p.streamk, p.force_slices, p.remainder, pull_d_env, head_env);
     if (plan.status != 0) return kTcErrShape;
     const int mode = plan.mode;
     const bool sk = mode != 0;
     if (dry_run) {
-        g_last = TcLaunchInfo{plan.clusters * kCluster, plan.clusters, mode, plan.sk_w > 0 ? 1 : 0};
+        g_last = TcLaunchInfo{plan.clusters * kCluster, plan.clusters, mode, plan.sk_pull ? 2 : plan.sk_w > 0 ? 1 : 0};
         return kTcOk;
     }
     if (sk) {
@@ -183,6 +202,8 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         args.sk_w = plan.sk_w;
         args.sk_extra = plan.sk_extra;
         args.sk_q = plan.sk_q;
+        args.sk_pull = plan.sk_pull;
+        args.sk_head = plan.sk_head;
         TcWorkspace* ws = p.workspace ? p.workspace : shared_workspace();
         const size_t slots = static_cast<size_t>(plan.slots);
         const size_t need_p = slots * kCtaGroup * S::WS_FLOATS;
@@ -208,7 +229,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     }
     clusters = plan.clusters;
     lc.gridDim = dim3(clusters * kCluster, 1, 1);
-    g_last = TcLaunchInfo{clusters * kCluster, clusters, mode, plan.sk_w > 0 ? 1 : 0};
+    g_last = TcLaunchInfo{clusters * kCluster, clusters, mode, plan.sk_pull ? 2 : plan.sk_w > 0 ? 1 : 0};
     // debugging aid: FI_TC_TRACE=<file> records a per-unit timeline of this launch
     const char* trace_path = std::getenv("FI_TC_TRACE");
     static unsigned long long* trace_buf = nullptr;
@@ -226,11 +247,12 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         if (FILE* f = std::fopen(trace_path, "a")) {
             std::fprintf(f, "launch ctas %d cluster %d mode %d tiles %d kb %d\n", clusters * kCluster, kCluster,
                          args.streamk, tiles, kb);
-            // cta unit t0 t1 t2 t3 clk0 clk1 t4 t5 t6 (globaltimer ns, clock64 of events 0/1)
+            // cta unit t0 t1 t2 t3 clk0 clk1 t4 t5 t6 clk2 clk6 (globaltimer ns, clock64)
             for (size_t i = 0; i < trace_n; i += 16)
                 if (h[i] || h[i + 2])
-                    std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 256, (i / 16) % 16,
-                                 h[i], h[i + 1], h[i + 2], h[i + 3], h[i + 8], h[i + 9], h[i + 4], h[i + 5], h[i + 6]);
+                    std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 256,
+                                 (i / 16) % 16, h[i], h[i + 1], h[i + 2], h[i + 3], h[i + 8], h[i + 9], h[i + 4], h[i + 5],
+                                 h[i + 6], h[i + 10], h[i + 14]);
             std::fclose(f);
         }
     }

@@ -172,6 +172,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
+            // L2 policy (args.l2_hint): 1 = A panels evict-last (a raster band re-reads
+            // them every wave) and B evict-first; 2 = the opposite
+            const uint64_t pol_a = args.l2_hint == 1 ? kL2EvictLast : args.l2_hint == 2 ? kL2EvictFirst : kL2EvictNormal;
+            const uint64_t pol_b = args.l2_hint == 1 ? kL2EvictFirst : args.l2_hint == 2 ? kL2EvictLast : kL2EvictNormal;
             UnitIter<BN> units(args, cluster, nclusters);
             Unit u;
             while (units.next(u)) {
@@ -196,21 +200,26 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     uint8_t* sb = sa + S::A_BYTES;
                     const int k0 = (kb0 + kb) * S::BK;
                     if (mma_leader) mbar_arrive_expect_tx(&full_bar[s], tx);
-                    auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
-                        if constexpr (kCtaGroup == 1) tma_load_2d(dst, map, &full_bar[s], c0, c1);
-                        else tma_load_2d_pair(dst, map, &full_bar[s], c0, c1);
+                    auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol) {
+                        if (args.l2_hint) {
+                            if constexpr (kCtaGroup == 1) tma_load_2d_hint(dst, map, &full_bar[s], c0, c1, pol);
+                            else tma_load_2d_pair_hint(dst, map, &full_bar[s], c0, c1, pol);
+                        } else {
+                            if constexpr (kCtaGroup == 1) tma_load_2d(dst, map, &full_bar[s], c0, c1);
+                            else tma_load_2d_pair(dst, map, &full_bar[s], c0, c1);
+                        }
                     };
                     if (args.a_mn_major) {
-                        load(sa, &tmA, m0, k0);
-                        load(sa + 8192, &tmA, m0 + 64, k0);
+                        load(sa, &tmA, m0, k0, pol_a);
+                        load(sa + 8192, &tmA, m0 + 64, k0, pol_a);
                     } else {
-                        load(sa, &tmA, k0, m0);
+                        load(sa, &tmA, k0, m0, pol_a);
                     }
                     if (args.b_mn_major) {
                         for (int j = 0; j < b_rows / 64; ++j)
-                            load(sb + j * 8192, &tmB, n0 + j * 64, k0);
+                            load(sb + j * 8192, &tmB, n0 + j * 64, k0, pol_b);
                     } else {
-                        load(sb, half ? &tmB2 : &tmB, k0, n0);  // tmB2: box of BN_LOCAL/2 rows
+                        load(sb, half ? &tmB2 : &tmB, k0, n0, pol_b);  // tmB2: box of BN_LOCAL/2 rows
                     }
                     if (++s == nst) { s = 0; ph ^= 1; }
                 }
@@ -313,7 +322,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             const uint32_t use = static_cast<uint32_t>(it >> 1);
             const uint32_t tile_use = static_cast<uint32_t>(it);
             ++it;
-            mbar_wait(&tfull_bar[buf], use & 1);
+            if (args.epi_sleep_ns) mbar_wait_sleep(&tfull_bar[buf], use & 1, args.epi_sleep_ns);
+            else mbar_wait(&tfull_bar[buf], use & 1);
             if (q == 0 && lane == 0) trace_stamp(args, it - 1, 2);
             tc_fence_after();
             const int m = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM + row;
@@ -376,6 +386,103 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                         store_row32_any(args, m, tn * BN + u.n_off + c * 32, v);
                     }
                     release_tmem();
+                } else if (args.sk_pull) {
+                    // 2-slice pull fixup. Slice 1 (K-blocks [0, w)) publishes its whole
+                    // partial; slice 0 ([w, kb)) streams it back chunk by chunk into
+                    // the epi buffers, adds it and stores C. As the cluster's last
+                    // unit (ring idle) slice 0 is longer by the publish time and
+                    // both stage through the ring; as its first unit (args.sk_head:
+                    // the ring feeds the next main loop) the halves are equal, the
+                    // publisher stages through the epi buffers and the owner stores
+                    // C from registers -- the exchange overlaps the next tiles.
+                    constexpr int NCH = BN / 32;
+                    constexpr uint32_t kChunkFloats = 32 * S::BM;
+                    constexpr uint32_t kChunkBytes = kChunkFloats * 4;
+                    const int rest = args.tiles_m * args.tiles_n - args.sk_tile_begin;
+                    const int tile_idx = u.tile - args.sk_tile_begin;
+                    float* stage0 = reinterpret_cast<float*>(ring);
+                    if (u.slice == 1) {
+                        float* slot_ws = args.workspace + static_cast<long>(u.slot * kCtaGroup + pair_rank) * S::WS_FLOATS;
+                        if (!args.sk_head) {
+                            drain_pairs(tbase, NCH, [&](int c) { return stage0 + c * kChunkFloats; },
+                                        [&](int c) { bulk_copy_s2g(slot_ws + c * kChunkFloats, stage0 + c * kChunkFloats, kChunkBytes); });
+                        } else {
+#pragma unroll 1
+                            for (int c = 0; c < NCH; ++c) {
+                                uint32_t r[32];
+                                tmem_ld_32x32b_x32(tbase + c * 32, r);
+                                float* stage = epi + (epi_chunk++ & 1) * kChunkFloats;
+                                if (q == 0 && lane == 0) bulk_wait_group_read<1>();
+                                epilogue_bar();
+                                tmem_ld_wait();
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) stage[j * S::BM + row] = __uint_as_float(r[j]);
+                                fence_proxy_async();
+                                epilogue_bar();
+                                if (q == 0 && lane == 0) {
+                                    bulk_copy_s2g(slot_ws + c * kChunkFloats, stage, kChunkBytes);
+                                    bulk_commit_group();
+                                }
+                            }
+                        }
+                        release_tmem();
+                        if (q == 0 && lane == 0) {
+                            bulk_wait_group<0>();
+                            fence_proxy_async_global();
+                            trace_stamp(args, it - 1, 4);
+                            st_release_gpu(args.flags + (u.slot * kCtaGroup + pair_rank), args.epoch);
+                        }
+                        __syncwarp();
+                    } else {
+                        const int ps = tile_idx + rest;  // slot of slice 1
+                        const float* peer_ws = args.workspace + static_cast<long>(ps * kCtaGroup + pair_rank) * S::WS_FLOATS;
+                        const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
+                        if (q == 0 && lane == 0) {
+                            while (ld_acquire_gpu(args.flags + (ps * kCtaGroup + pair_rank)) < args.epoch) __nanosleep(64);
+                            fence_proxy_async_global();
+                            trace_stamp(args, it - 1, 4);
+                            bulk_wait_group_read<0>();  // earlier units' C stores have left the epi buffers
+                            for (int c = 0; c < 2; ++c) {  // prefetch chunks 0, 1 into the epi buffers
+                                mbar_arrive_expect_tx(&stage_bar[c], kChunkBytes);
+                                bulk_copy_g2s(epi + c * kChunkFloats, peer_ws + c * kChunkFloats, kChunkBytes, &stage_bar[c]);
+                            }
+                        }
+                        __syncwarp();
+#pragma unroll 1
+                        for (int c = 0; c < NCH; ++c) {
+                            uint32_t r[32];
+                            tmem_ld_32x32b_x32(tbase + c * 32, r);
+                            const int b = c & 1;
+                            mbar_wait(&stage_bar[b], static_cast<uint32_t>(c >> 1) & 1);
+                            tmem_ld_wait();
+                            const float* pp = epi + b * kChunkFloats + row;
+                            float v[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) v[j] = pp[j * S::BM] + __uint_as_float(r[j]);
+                            epilogue_bar();  // every thread has read epi[b]: refill it with chunk c + 2
+                            if (q == 0 && lane == 0 && c + 2 < NCH) {
+                                fence_proxy_async();
+                                mbar_arrive_expect_tx(&stage_bar[b], kChunkBytes);
+                                bulk_copy_g2s(epi + b * kChunkFloats, peer_ws + (c + 2) * kChunkFloats, kChunkBytes,
+                                              &stage_bar[b]);
+                            }
+                            if (args.c_tma && !args.sk_head) {
+                                float* dst = stage0 + c * kChunkFloats + row;
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) dst[j * S::BM] = v[j];
+                                fence_proxy_async();
+                                epilogue_bar();
+                                if (q == 0 && lane == 0) {
+                                    tma_store_2d(&tmC, stage0 + c * kChunkFloats, m_cta, tn * BN + c * 32);
+                                    bulk_commit_group();
+                                }
+                            } else {
+                                store_row32_any(args, m, tn * BN + c * 32, v);
+                            }
+                        }
+                        release_tmem();
+                        if (q == 0 && lane == 0) trace_stamp(args, it - 1, 5);
+                    }
                 } else {
                     // K-slice tail unit. Symmetric fixup: main slice s owns 32-column
                     // chunks [c_lo, c_hi) and keeps those in smem (a main slice is the

@@ -40,8 +40,19 @@ struct GemmArgs {
     int sk_w = 0;
     int sk_extra = 0;
     int sk_q = 0;
+    // 2-slice pull fixup (K-slice tail with S = 2, no remainder): slice 1 runs
+    // K-blocks [0, sk_w) and publishes its whole partial; slice 0 runs the longer
+    // [sk_w, k_blocks) -- its extra MMA time hides the publish -- then streams
+    // the partial in chunk by chunk, adds it and stores C
+    int sk_pull = 0;
+    // tail units first (sk_pull only): each cluster runs its K-slice unit before
+    // its data-parallel tiles, so the fixup's partial exchange and C stores
+    // overlap the following main loops instead of ending the kernel exposed
+    int sk_head = 0;
     int c_tma = 0;                   // f32 col-major C stored by TMA from smem staging
     int ring_drain = 1;              // the cluster's last unit stages C in the idle operand ring
+    unsigned epi_sleep_ns = 256;     // epilogue polls the accumulator barrier every N ns (0: try_wait)
+    int l2_hint = 0;                 // TMA L2 eviction policy: 0 normal, 1 A last / B first, 2 A first / B last
     float* workspace = nullptr;     // [slots][kCtaGroup][BN][128] fp32 partials
     unsigned* flags = nullptr;       // [slots][kCtaGroup] epoch of the published partial
                                      // slots: one per cluster + sk_extra*(sk_q-1)
@@ -155,6 +166,7 @@ struct UnitIter {
         step = nclusters;
     }
     FI_HD bool next(Unit& u) {
+        if (args->sk_head && tail_unit >= 0) return take_tail(u);
         if (t < dp_tiles) {
             u = Unit{t, 0, kb, 0, BN, 0, 0};
             t += step;
@@ -169,6 +181,10 @@ struct UnitIter {
             ++rem_j;
             return true;
         }
+        return take_tail(u);
+    }
+    // the cluster's K-slice / N-split unit of a leftover tile
+    FI_HD bool take_tail(Unit& u) {
         const int s = tail_unit / rest;
         u.tile = dp_tiles + tail_unit % rest;
         u.slice = s;
@@ -178,6 +194,11 @@ struct UnitIter {
             u.k1 = kb;
             u.width = BN / 2;
             u.n_off = s * (BN / 2);
+        } else if (args->sk_pull) {  // 2-slice pull fixup: slice 1 publishes [0, w), slice 0 owns [w, kb)
+            u.k0 = s == 0 ? w : 0;
+            u.k1 = s == 0 ? kb : w;
+            u.n_off = 0;
+            u.width = BN;
         } else if (w > 0) {  // K-slice s of a tail with a remainder slice
             u.k0 = s * w;
             u.k1 = (s + 1) * w;
@@ -203,13 +224,13 @@ struct SchedulePlan {
     int clusters = 0;      // clusters launched
     int mode = 0;          // 0 data-parallel, 1 K-slice tail, 2 N-split tail
     int slices = 1, sk_begin = 0;
-    int sk_w = 0, sk_extra = 0, sk_q = 0;
+    int sk_w = 0, sk_extra = 0, sk_q = 0, sk_pull = 0, sk_head = 0;
     long slots = 0;        // workspace slots (partials + flags), 0 without a tail split
 };
 
 template <int kCtaGroup, int BN, int kSplitK>
 inline SchedulePlan plan_schedule(int tiles, int kb, int clusters, bool b_mn_major, int streamk,
-                                  int force_slices, int remainder) {
+                                  int force_slices, int remainder, int pull_d = -1, int head = 0) {
     using S = GemmShape<kCtaGroup, BN, kSplitK>;
     SchedulePlan P;
     // Tail split: whole waves data-parallel; the R leftover tiles of the partial
@@ -271,6 +292,19 @@ inline SchedulePlan plan_schedule(int tiles, int kb, int clusters, bool b_mn_maj
                 P.sk_q = q;
             }
         }
+    }
+    // pull fixup for 2-slice tails: the publisher's share is shorter by the
+    // time its 128 KB/CTA publish takes (~pull_d K-blocks at the per-SM write
+    // rate), so the owner's MMA covers it
+    // (or, with head >= 1 and data-parallel tiles to follow, equal halves run
+    // first so the whole fixup overlaps the next main loops)
+    if (mode == 1 && slices == 2 && P.sk_w == 0 && pull_d >= 0 && kb >= 24) {
+        const bool head_ok = head > 0 && sk_begin > 0;
+        int w = head_ok ? kb / 2 : (kb - pull_d) / 2;
+        if (w < 8) w = 8;
+        P.sk_pull = 1;
+        P.sk_head = head_ok ? 1 : 0;
+        P.sk_w = w;
     }
     P.mode = mode;
     P.slices = slices;

@@ -56,7 +56,7 @@ struct TcWorkspace {
 
 struct TcLaunchInfo {
     int ctas = 0, clusters = 0, streamk = 0;
-    int remainder = 0;  // K-slice tail with a remainder slice
+    int remainder = 0;  // K-slice tail: 1 remainder slices, 2 two-slice pull fixup
 };
 TcLaunchInfo tc_gemm_last_launch();
 

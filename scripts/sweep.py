@@ -52,12 +52,15 @@ def time_plan(plan, steps, flush):
     return statistics.median(ts)
 
 
-def time_cublas(m, n, k, steps, flush):
+def time_cublas(m, n, k, steps, flush, out_dtype=torch.float32):
     """Library reference (not part of the product): cuBLAS through torch.mm on
-    the same col-major problem, f16 in / f32 accumulate / f16 out."""
+    the same col-major problem, f16 in / f32 accumulate / f32 (or f16) out."""
     a = torch.rand((k, m), device="cuda").half() - 0.5   # col-major A = row-major A^T
     b = torch.rand((n, k), device="cuda").half() - 0.5
-    f = lambda: torch.mm(b, a)                              # C^T (N x M) row-major = C col-major
+    if out_dtype == torch.float16:
+        f = lambda: torch.mm(b, a)                          # C^T (N x M) row-major = C col-major
+    else:
+        f = lambda: torch.mm(b, a, out_dtype=out_dtype)
     for _ in range(3):
         f()
     s = torch.cuda.current_stream()
@@ -103,11 +106,12 @@ def main():
                                            "streamk": int(plan.info.streamk), "ctas": int(plan.info.launch_ctas)}
             except Exception as e:  # noqa: BLE001
                 row["strategies"][name] = {"error": str(e)[:200]}
-        try:
-            ms = time_cublas(m, n, k, args.steps, flush)
-            row["cublas_f16out"] = {"ms": ms, "tflops": row["flops"] / ms / 1e9}
-        except Exception as e:  # noqa: BLE001
-            row["cublas_f16out"] = {"error": str(e)[:200]}
+        for key, odt in (("cublas_f32out", torch.float32), ("cublas_f16out", torch.float16)):
+            try:
+                ms = time_cublas(m, n, k, args.steps, flush, odt)
+                row[key] = {"ms": ms, "tflops": row["flops"] / ms / 1e9}
+            except Exception as e:  # noqa: BLE001
+                row[key] = {"error": str(e)[:200]}
         ok = {k2: v for k2, v in row["strategies"].items() if "tflops" in v}
         if ok:
             best = max(ok, key=lambda x: ok[x]["tflops"])
@@ -117,7 +121,8 @@ def main():
             row["ceiling_tflops"] = min(pk, ai * 6531.6e9 / 1e12)
         results.append(row)
         print(f"{kind:6s} {m:5d}x{n:5d}x{k:5d}  best {row.get('best', '-'):24s} {row.get('best_tflops', 0):8.1f} TF"
-              f"  (ceiling {row.get('ceiling_tflops', 0):7.1f}, cuBLAS {row['cublas_f16out'].get('tflops', 0):7.1f})  " +
+              f"  (ceiling {row.get('ceiling_tflops', 0):7.1f}, cuBLAS f32/f16 out {row['cublas_f32out'].get('tflops', 0):7.1f}"
+              f"/{row['cublas_f16out'].get('tflops', 0):7.1f})  " +
               "  ".join(f"{a}={v.get('tflops', float('nan')):.0f}" for a, v in row["strategies"].items()),
               flush=True)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)

@@ -19,6 +19,8 @@ def main(path):
                 cur.setdefault("fix", []).append((vals[4], vals[8], vals[9], vals[5]))
                 if len(vals) >= 11 and vals[10]:
                     cur.setdefault("drain", []).append((vals[10] - vals[4], vals[8] - vals[10]))
+                if len(vals) >= 13 and vals[12] and vals[11]:
+                    cur.setdefault("drain_clk", []).append(vals[12] - vals[11])
             if len(vals) >= 8 and vals[6] and vals[7] and vals[3] > vals[2]:
                 cur.setdefault("mhz", []).append((vals[7] - vals[6]) / (vals[3] - vals[2]) * 1e3)
     last = launches[-1]
@@ -55,6 +57,9 @@ def main(path):
         print(f"tail fixup (median / max us): acc ready->partial published {med(pub):.2f} / {max(pub):.2f}  "
               f"published->peers staged {med(stg):.2f} / {max(stg) if stg else 0:.2f}  "
               f"staged->stored {med(fin):.2f} / {max(fin) if fin else 0:.2f}  (n={len(fix)}, owners={len(stg)})")
+        dc = last.get("drain_clk")
+        if dc:
+            print(f"  TMEM->SMEM drain in SM cycles (clock64): median {statistics.median(dc):.0f}, max {max(dc)}")
         dr = last.get("drain")
         if dr:
             print(f"  of which TMEM->SMEM drain {med([d[0] / 1e3 for d in dr]):.2f} us, "

@@ -32,9 +32,9 @@ def test_remainder_tail_exact_and_deterministic(fi, oracle, monkeypatch, m, n, k
     script = fi.strategies.tc_strategy(m, n, k, **kw)
     plan = _plan(fi, script, True, monkeypatch)
     assert plan.kind == "tcgen05"
-    assert bool(plan.info.remainder) == expect
+    assert (plan.info.remainder == 1) == expect
     even = _plan(fi, script, False, monkeypatch)
-    assert not even.info.remainder
+    assert even.info.remainder != 1
     # integer inputs: exact at 4096 sampled fp64 dot products, and bitwise equal
     # to the even-slice schedule over the whole matrix (both are exact)
     a = oracle.fill(m, k, 11, True)
