@@ -126,11 +126,6 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         return v ? std::atoi(v) : 0;
     }();
     args.l2_hint = l2_hint_env;
-    static const int epi_sleep_env = [] {
-        const char* v = std::getenv("FI_TC_EPI_SLEEP");
-        return v ? std::atoi(v) : 256;
-    }();
-    args.epi_sleep_ns = static_cast<unsigned>(epi_sleep_env);
 
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
@@ -247,12 +242,12 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         if (FILE* f = std::fopen(trace_path, "a")) {
             std::fprintf(f, "launch ctas %d cluster %d mode %d tiles %d kb %d\n", clusters * kCluster, kCluster,
                          args.streamk, tiles, kb);
-            // cta unit t0 t1 t2 t3 clk0 clk1 t4 t5 t6 clk2 clk6 (globaltimer ns, clock64)
+            // cta unit t0 t1 t2 t3 clk0 clk1 t4 t5 t6 clk2 clk6 t7 (globaltimer ns, clock64)
             for (size_t i = 0; i < trace_n; i += 16)
                 if (h[i] || h[i + 2])
-                    std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 256,
+                    std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 256,
                                  (i / 16) % 16, h[i], h[i + 1], h[i + 2], h[i + 3], h[i + 8], h[i + 9], h[i + 4], h[i + 5],
-                                 h[i + 6], h[i + 10], h[i + 14]);
+                                 h[i + 6], h[i + 10], h[i + 14], h[i + 7]);
             std::fclose(f);
         }
     }

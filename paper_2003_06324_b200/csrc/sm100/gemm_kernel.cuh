@@ -135,6 +135,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     const bool mma_leader = pair_rank == 0;
     const uint16_t pair_mask = static_cast<uint16_t>(3u << (crank - pair_rank));
 
+    if (threadIdx.x == 0 && args.trace) {  // kernel entry (event 7 of unit 0)
+        args.trace[(blockIdx.x * 16) * 16 + 7] = global_timer_ns();
+        args.trace[(blockIdx.x * 16) * 16 + 15] = clock64();
+    }
     if (threadIdx.x == 32) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -322,8 +326,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             const uint32_t use = static_cast<uint32_t>(it >> 1);
             const uint32_t tile_use = static_cast<uint32_t>(it);
             ++it;
-            if (args.epi_sleep_ns) mbar_wait_sleep(&tfull_bar[buf], use & 1, args.epi_sleep_ns);
-            else mbar_wait(&tfull_bar[buf], use & 1);
+            mbar_wait(&tfull_bar[buf], use & 1);
             if (q == 0 && lane == 0) trace_stamp(args, it - 1, 2);
             tc_fence_after();
             const int m = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM + row;

@@ -88,27 +88,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-// Low-power wait for long phases: a non-blocking test every `ns` nanoseconds.
-// try_wait's suspended warps are woken by every barrier update of the CTA (the
-// TMA/MMA ring completes one per K-block), so an epilogue parked on the
-// accumulator barrier through a whole main loop re-polls every ~75 cycles
-// (7.9M polls per 8192^3 launch, profiles/round1/): issue slots and power the
-// tensor cores need under the 1 kW cap.
-__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
-    while (!mbar_test_wait(bar, parity)) __nanosleep(ns);
-}
-
 // Cluster-scope acquire: pairs with remote release arrivals from peer CTAs.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
     asm volatile(

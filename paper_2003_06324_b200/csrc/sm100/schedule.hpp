@@ -51,7 +51,6 @@ struct GemmArgs {
     int sk_head = 0;
     int c_tma = 0;                   // f32 col-major C stored by TMA from smem staging
     int ring_drain = 1;              // the cluster's last unit stages C in the idle operand ring
-    unsigned epi_sleep_ns = 256;     // epilogue polls the accumulator barrier every N ns (0: try_wait)
     int l2_hint = 0;                 // TMA L2 eviction policy: 0 normal, 1 A last / B first, 2 A first / B last
     float* workspace = nullptr;     // [slots][kCtaGroup][BN][128] fp32 partials
     unsigned* flags = nullptr;       // [slots][kCtaGroup] epoch of the published partial

@@ -21,6 +21,8 @@ def main(path):
                     cur.setdefault("drain", []).append((vals[10] - vals[4], vals[8] - vals[10]))
                 if len(vals) >= 13 and vals[12] and vals[11]:
                     cur.setdefault("drain_clk", []).append(vals[12] - vals[11])
+                if len(vals) >= 14 and vals[13] and vals[1] == 0:
+                    cur.setdefault("entry", []).append((vals[13], vals[2]))
             if len(vals) >= 8 and vals[6] and vals[7] and vals[3] > vals[2]:
                 cur.setdefault("mhz", []).append((vals[7] - vals[6]) / (vals[3] - vals[2]) * 1e3)
     last = launches[-1]
@@ -31,6 +33,12 @@ def main(path):
     t0 = min(r[2] for r in rows if r[2])
     end = max(max(r[3], r[5]) for r in rows)
     print(last["hdr"], f"span {(end - t0) / 1e3:.1f} us, {len(set(r[0] for r in rows))} CTAs")
+    if last.get("entry"):
+        e0 = min(e for e, _ in last["entry"])
+        lag = [(p - e) / 1e3 for e, p in last["entry"] if p]
+        print(f"kernel entry: CTAs enter over {(max(e for e, _ in last['entry']) - e0) / 1e3:.2f} us; entry -> first "
+              f"TMA load median {statistics.median(lag):.2f} us, max {max(lag):.2f}; first entry -> last stamp "
+              f"{(end - e0) / 1e3:.1f} us")
     per_cta = {}
     for cta, unit, p0, m1, e2, e3 in rows:
         per_cta.setdefault(cta, []).append((unit, p0, m1, e2, e3))
