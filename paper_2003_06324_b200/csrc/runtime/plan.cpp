@@ -495,6 +495,7 @@ std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const 
         info.shared_bytes = sm100::tc_gemm_smem_bytes(c);
         if (const char* e = std::getenv("FI_STREAMK")) p.streamk = std::atoi(e);
         if (const char* e = std::getenv("FI_REMAINDER")) p.remainder = std::atoi(e);
+        if (const char* e = std::getenv("FI_TC_MAX_CTAS")) p.max_ctas = std::atoi(e);  // experiments: smaller grid
         const sm100::TcLaunchInfo li = sm100::tc_gemm_plan(c, p);
         info.launch_ctas = li.ctas;
         info.streamk = li.streamk;
