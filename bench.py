@@ -65,6 +65,8 @@ def workload_of(args, world):
 def strategy_for(fi, wl, m, n, k):
     if wl["name"].startswith("c3"):
         return fi.strategies.c3_strategy()
+    if wl["name"].startswith("c5"):
+        return fi.strategies.c5_strategy(m, n, k)  # per-shard shape under torchrun
     return fi.strategies.tc_strategy(m, n, k, ab=wl["ab"], pair=True, tile_n=256)
 
 

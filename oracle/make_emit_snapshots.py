@@ -20,6 +20,7 @@ CASES = {
     "reuse_buffer": lambda: (ROOT / "tests/fixtures/reuse_buffer.fi").read_text(),
     "c2_tcgen05": fi.strategies.c2_strategy,
     "c3_splitk": fi.strategies.c3_strategy,
+    "pair512_slabs": lambda: fi.strategies.tc_strategy(8192, 8192, 8192, tile_m=512),
 }
 
 if __name__ == "__main__":

@@ -120,11 +120,12 @@ const char* role_name(int r) {
     return n[r];
 }
 
-template <int kCtaGroup, int BN, int kSplitK>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1>
 class Checker {
-    using S = GemmShape<kCtaGroup, BN, kSplitK>;
+    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs>;
     static constexpr int kStages = S::kStages;
     static constexpr int NCH = BN / 32;
+    static constexpr int NCH_ALL = NCH * kSlabs;  // 32-column chunks of a tile's CTA rows, all slabs
     static constexpr int kChunkBytes = 32 * S::BM * 4;
     static constexpr int kGran = 1024;  // shared-memory cell granularity (bytes)
 
@@ -189,12 +190,12 @@ public:
         // coverage: every 32-column chunk of every tile's CTA rows stored exactly once
         const long tiles = static_cast<long>(a_.tiles_m) * a_.tiles_n;
         for (long t = 0; t < tiles; ++t)
-            for (int ch = 0; ch < NCH; ++ch) {
-                auto it = stores_.find(t * NCH + ch);
+            for (int ch = 0; ch < NCH_ALL; ++ch) {
+                auto it = stores_.find(t * NCH_ALL + ch);
                 const int n = it == stores_.end() ? 0 : it->second;
                 if (n != 1) {
                     ++rep_.coverage_errors;
-                    record("coverage", "C", t * NCH + ch, "tile " + std::to_string(t) + " chunk " +
+                    record("coverage", "C", t * NCH_ALL + ch, "tile " + std::to_string(t) + " chunk " +
                            std::to_string(ch) + " stored " + std::to_string(n) + " times", "", -1);
                 }
             }
@@ -218,7 +219,7 @@ private:
     std::vector<Cta> ctas_;
     std::vector<Flag> flags_;
     std::unordered_map<uint64_t, Cell> cells_;
-    std::unordered_map<long, int> stores_;  // (tile*NCH + chunk) -> times stored
+    std::unordered_map<long, int> stores_;  // (tile*NCH_ALL + chunk) -> times stored
 
     int agent(int cta, int role) const { return cta * kRoles + role; }
     int cta_of(int c, int r) const { return c * kSplitK + r; }
@@ -289,12 +290,12 @@ private:
         for (long x = off / kGran; x < (off + bytes + kGran - 1) / kGran; ++x) access(ag, space, cta, x, write);
     }
     void tmem(int ag, int cta, int buf, int col0, int cols, bool write) {
-        if (col0 < 0 || col0 + cols > BN) {
+        if (col0 < 0 || col0 + cols > S::ACC_COLS || buf >= S::kAccBufs) {
             ++rep_.capacity_errors;
             record("capacity", "tmem", col0, "columns beyond the accumulator", who(ag), cta);
             return;
         }
-        for (int ch = col0 / 32; ch < (col0 + cols) / 32; ++ch) access(ag, kTmem, cta, buf * NCH + ch, write);
+        for (int ch = col0 / 32; ch < (col0 + cols) / 32; ++ch) access(ag, kTmem, cta, buf * NCH_ALL + ch, write);
     }
     void workspace(int ag, long slot, int ch0, int nch, bool write) {
         if (slot < 0 || slot >= slots_) {
@@ -305,8 +306,8 @@ private:
         for (int ch = ch0; ch < ch0 + nch; ++ch) access(ag, kWs, 0, static_cast<uint64_t>(slot) * NCH + ch, write);
     }
     void store_c(int ag, int tile, int ch) {
-        access(ag, kC, 0, static_cast<uint64_t>(tile) * NCH + ch, true);
-        ++stores_[static_cast<long>(tile) * NCH + ch];
+        access(ag, kC, 0, static_cast<uint64_t>(tile) * NCH_ALL + ch, true);
+        ++stores_[static_cast<long>(tile) * NCH_ALL + ch];
     }
 
     // ---- synchronisation
@@ -411,8 +412,8 @@ private:
         UnitIter<BN> units(a_, cl, ncl_);
         Unit u;
         while (units.next(u)) {
-            const int buf = it & 1;
-            const uint32_t use = static_cast<uint32_t>(it >> 1);
+            const int buf = S::kAccBufs == 2 ? (it & 1) : 0;
+            const uint32_t use = static_cast<uint32_t>(S::kAccBufs == 2 ? (it >> 1) : it);
             ++it;
             if (opt_.mutation != kMutSkipTmemEmptyWait) {
                 co_await wait(C.tempty[buf], (use & 1) ^ 1);
@@ -425,7 +426,7 @@ private:
                 ++vc_[static_cast<size_t>(M)][static_cast<size_t>(M)];
                 issue(X, M);
                 smem(X, cta, kRing, static_cast<long>(s) * S::STAGE_BYTES, bytes, false);
-                tmem(X, cta, buf, 0, u.width, true);
+                tmem(X, cta, buf, 0, u.width * kSlabs, true);
                 arrive(C.empty[static_cast<size_t>(s)], vc_[static_cast<size_t>(X)]);  // tcgen05.commit
                 if (++s == nst_) {
                     s = 0;
@@ -459,48 +460,51 @@ private:
         while (have) {
             const bool have_next = units.next(nxt);
             const bool last_unit = !have_next || opt_.mutation == kMutRingDrainEveryUnit;
-            const int buf = it & 1;
-            const uint32_t use = static_cast<uint32_t>(it >> 1);
+            const int buf = S::kAccBufs == 2 ? (it & 1) : 0;
+            const uint32_t use = static_cast<uint32_t>(S::kAccBufs == 2 ? (it >> 1) : it);
             const uint32_t tile_use = static_cast<uint32_t>(it);
             ++it;
             co_await wait(C.tfull[buf], use & 1);
             acquire(E, C.tfull[buf], use & 1);
             const int tile = u.tile;
             const int ch_off = u.n_off / 32;
+            const int nchu = u.width / 32, nch_all = nchu * kSlabs;
+            auto cchunk = [&](int c) { return (c / nchu) * NCH + ch_off + c % nchu; };  // C chunk id of TMEM chunk c
             auto release_tmem = [&] {
                 tick();
                 arrive(C.tempty[buf], ve);
             };
             if constexpr (kSplitK == 1) {
                 const bool whole = u.k0 == 0 && u.k1 == kb;
-                if (whole && a_.c_tma && last_unit && a_.ring_drain) {
+                if (whole && a_.c_tma && last_unit && a_.ring_drain &&
+                    static_cast<long>(nch_all) * kChunkBytes <= S::RING_BYTES) {
                     // ring-staged last unit: chunks at ring + c*16KB, TMA-stored pairwise
-                    for (int c = 0; c < u.width / 32; ++c) {
+                    for (int c = 0; c < nch_all; ++c) {
                         tmem(E, cta, buf, c * 32, 32, false);
                         smem(E, cta, kRing, static_cast<long>(c) * kChunkBytes, kChunkBytes, true);
                         if (c & 1) {
                             for (int x = c - 1; x <= c; ++x)
                                 bulk_store(kRing, static_cast<long>(x) * kChunkBytes,
-                                           [&](int bw) { store_c(bw, tile, ch_off + x); });
+                                           [&](int bw) { store_c(bw, tile, cchunk(x)); });
                             commit_group(cta);
                         }
                     }
                     release_tmem();
                 } else if (whole && a_.c_tma) {
                     // double-buffered epi staging, one TMA store per chunk
-                    for (int c = 0; c < u.width / 32; ++c) {
+                    for (int c = 0; c < nch_all; ++c) {
                         tmem(E, cta, buf, c * 32, 32, false);
                         const long off = static_cast<long>(epi_chunk++ & 1) * kChunkBytes;
                         wait_groups(cta, 1, false);  // bulk_wait_group_read<1> + epilogue_bar
                         smem(E, cta, kEpi, off, kChunkBytes, true);
-                        bulk_store(kEpi, off, [&](int bw) { store_c(bw, tile, ch_off + c); });
+                        bulk_store(kEpi, off, [&](int bw) { store_c(bw, tile, cchunk(c)); });
                         commit_group(cta);
                     }
                     release_tmem();
                 } else if (whole) {
-                    for (int c = 0; c < u.width / 32; ++c) {
+                    for (int c = 0; c < nch_all; ++c) {
                         tmem(E, cta, buf, c * 32, 32, false);
-                        store_c(E, tile, ch_off + c);
+                        store_c(E, tile, cchunk(c));
                     }
                     release_tmem();
                 } else if (a_.sk_pull) {
@@ -687,17 +691,20 @@ private:
     }
 };
 
-template <int kCtaGroup, int BN, int kSplitK>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1>
 void run_checker(GemmArgs args, int sms, int force_slices, const AsyncCheckOptions& o, AsyncReport& rep) {
-    using S = GemmShape<kCtaGroup, BN, kSplitK>;
+    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs>;
     constexpr int kCluster = kCtaGroup * kSplitK;
     const int tiles = args.tiles_m * args.tiles_n;
     int clusters = sms / kCluster;
     if (o.max_active_clusters > 0 && o.max_active_clusters < clusters) clusters = o.max_active_clusters;
-    const SchedulePlan plan = plan_schedule<kCtaGroup, BN, kSplitK>(tiles, args.k_blocks, clusters,
-                                                                    args.b_mn_major != 0, o.streamk,
-                                                                    force_slices, o.remainder,
-                                                                    o.pull_d == -2 ? BN / 32 : o.pull_d, o.head);
+    // as the launcher: slab tiles (512-row pair tiles) run whole tiles only
+    const SchedulePlan plan =
+        kSlabs > 1 ? plan_schedule<kCtaGroup, BN, kSplitK>(tiles, args.k_blocks, clusters, args.b_mn_major != 0, 0, 0,
+                                                           0, -1, 0)
+                   : plan_schedule<kCtaGroup, BN, kSplitK>(tiles, args.k_blocks, clusters, args.b_mn_major != 0,
+                                                           o.streamk, force_slices, o.remainder,
+                                                           o.pull_d == -2 ? BN / 32 : o.pull_d, o.head);
     rep.tiles = tiles;
     rep.cluster_size = kCluster;
     rep.split_k = kSplitK > 1 ? kSplitK : (force_slices > 1 ? force_slices : 1);
@@ -729,7 +736,7 @@ void run_checker(GemmArgs args, int sms, int force_slices, const AsyncCheckOptio
         Unit u;
         while (it.next(u)) ++rep.units;
     }
-    Checker<kCtaGroup, BN, kSplitK> chk(args, plan.clusters, plan.slots, o, rep);
+    Checker<kCtaGroup, BN, kSplitK, kSlabs> chk(args, plan.clusters, plan.slots, o, rep);
     chk.run();
 }
 
@@ -741,7 +748,7 @@ AsyncReport check_async(const Spec& root, const NodePtr& tree, const AsyncCheckO
     if (!tc.matched) fail(ErrorKind::InvalidTree, "not a tcgen05 strategy: " + tc.why_not);
     const auto& mm = root.mm();
     // the launcher's configuration (runtime/plan.cpp Plan::create)
-    const int bm = 128 * tc.cta_group;
+    const int bm = tc.tile_m;  // 128, 256 (pair) or 512 (pair, two A slabs)
     const long M = root.m(), N = root.n(), K = root.k();
     int split_k = tc.split_k, force_slices = 0;
     if (M % bm || N % tc.tile_n || K % (64 * split_k))
@@ -765,6 +772,10 @@ AsyncReport check_async(const Spec& root, const NodePtr& tree, const AsyncCheckO
     a.c_tma = opts.c_tma >= 0 ? opts.c_tma : (split_k == 1 && a.out_type == 0 && !a.c_row_major ? 1 : 0);
     a.ring_drain = opts.ring_drain;
     AsyncReport rep;
+    if (tc.tile_m == 512) {
+        run_checker<2, 256, 1, 2>(a, opts.num_sms, force_slices, opts, rep);
+        return rep;
+    }
 #define FI_CHECK(CG, BN_, SK)                                                        \
     if (tc.cta_group == CG && tc.tile_n == BN_ && split_k == SK) {                 \
         run_checker<CG, BN_, SK>(a, opts.num_sms, force_slices, opts, rep);        \

@@ -326,8 +326,8 @@ KernelSource generate(const Program& prog) {
           << "namespace fi_generated {\n"
           << "using namespace fireiron::sm100;\n"
           << "constexpr int kCtaGroup = " << tc.cta_group << ", kTileN = " << tc.tile_n << ", kSplitK = " << tc.split_k
-          << ";\n"
-          << "using Shape = GemmShape<kCtaGroup, kTileN, kSplitK>;\n"
+          << ", kSlabs = " << tc.tile_m / (128 * tc.cta_group) << ";\n"
+          << "using Shape = GemmShape<kCtaGroup, kTileN, kSplitK, kSlabs>;\n"
           << "// grid: one persistent CTA per SM (clusters of kCtaGroup*kSplitK), "
           << "dynamic smem Shape::SMEM_BYTES\n"
           << "inline GemmArgs " << prog.entry_name << "_args(void* C) {\n"
@@ -348,7 +348,7 @@ KernelSource generate(const Program& prog) {
           << "(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,\n"
           << "    const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,\n"
           << "    const __grid_constant__ GemmArgs args) {\n"
-          << "  fi_sm100_gemm_body<kCtaGroup, kTileN, kSplitK>(tmA, tmB, tmB2, tmC, args);\n"
+          << "  fi_sm100_gemm_body<kCtaGroup, kTileN, kSplitK, kSlabs>(tmA, tmB, tmB2, tmC, args);\n"
           << "}\n"
           << "}  // namespace fi_generated\n";
         ks.source = o.str();
@@ -414,8 +414,10 @@ TcStrategy match_tc_strategy(const Spec& root, const NodePtr& tree, const MicroK
     tc.cta_group = blk->tile_ref.pair ? 2 : 1;
     tc.tile_m = static_cast<int>(blk->tile_r);
     tc.tile_n = static_cast<int>(blk->tile_c);
-    if (tc.tile_m != 128 * tc.cta_group)
-        return reject("block tile M must be 128 (or 256 with .pair): one TMEM lane per row");
+    // one TMEM lane per row: 128, 256 with .pair, or 512 with .pair and N = 256
+    // (two A slabs per CTA sharing B, the whole TMEM per accumulator)
+    if (tc.tile_m != 128 * tc.cta_group && !(tc.cta_group == 2 && tc.tile_m == 512))
+        return reject("block tile M must be 128, 256 with .pair, or 512 with .pair and N 256");
     if (tc.tile_n != 64 && tc.tile_n != 128 && tc.tile_n != 256) return reject("block tile N must be 64, 128 or 256");
     const DecompNode* nx = at(i++);
     if (nx && nx->kind == NodeKind::Split && nx->split_ref.splitk) {
@@ -466,6 +468,8 @@ TcStrategy match_tc_strategy(const Spec& root, const NodePtr& tree, const MicroK
     } catch (const Error& e) {
         return reject(e.what());
     }
+    if (tc.tile_m == 512 && (tc.tile_n != 256 || tc.split_k > 1))
+        return reject("512-row pair tiles need N = 256 and no split-K (their accumulator fills TMEM)");
     if (tc.split_k > 1) {
         const int cluster = tc.split_k * tc.cta_group;
         if (cluster > 8 || (tc.split_k != 2 && tc.split_k != 4))

@@ -102,11 +102,12 @@ __device__ __forceinline__ void epilogue_bar() { asm volatile("bar.sync 1, 128;"
 
 // Kernel body; the tensor maps must be __grid_constant__ kernel parameters
 // (TMA reads them through their parameter-space address).
-template <int kCtaGroup, int BN, int kSplitK>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs>
 __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                                    const CUtensorMap& tmB2, const CUtensorMap& tmC,
                                                    const GemmArgs& args) {
-    using S = GemmShape<kCtaGroup, BN, kSplitK>;
+    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs>;
+    static_assert(kSlabs == 1 || (kCtaGroup == 2 && kSplitK == 1), "A slabs pair with CTA pairs, no cluster split-K");
     constexpr int kStages = S::kStages;
     constexpr int kClusterSize = kCtaGroup * kSplitK;
 
@@ -213,11 +214,16 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                             else tma_load_2d_pair(dst, map, &full_bar[s], c0, c1);
                         }
                     };
-                    if (args.a_mn_major) {
-                        load(sa, &tmA, m0, k0, pol_a);
-                        load(sa + 8192, &tmA, m0 + 64, k0, pol_a);
-                    } else {
-                        load(sa, &tmA, k0, m0, pol_a);
+#pragma unroll
+                    for (int sl = 0; sl < kSlabs; ++sl) {  // slab sl: rows m0 + sl * BM_MMA
+                        uint8_t* sas = sa + sl * S::SLAB_BYTES;
+                        const int m0s = m0 + sl * S::BM_MMA;
+                        if (args.a_mn_major) {
+                            load(sas, &tmA, m0s, k0, pol_a);
+                            load(sas + 8192, &tmA, m0s + 64, k0, pol_a);
+                        } else {
+                            load(sas, &tmA, k0, m0s, pol_a);
+                        }
                     }
                     if (args.b_mn_major) {
                         for (int j = 0; j < b_rows / 64; ++j)
@@ -237,7 +243,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                                         (static_cast<uint32_t>(args.ab_format) << 10) |
                                         (static_cast<uint32_t>(args.a_mn_major) << 15) |
                                         (static_cast<uint32_t>(args.b_mn_major) << 16) |
-                                        (static_cast<uint32_t>(S::BM_TILE >> 4) << 24);
+                                        (static_cast<uint32_t>(S::BM_MMA >> 4) << 24);
             // K-major: rows of 128B, 8-row atoms 1024B apart (SBO), K step = 32B.
             // MN-major: 64-element chunks 8KB apart (LBO), 8 k-rows per atom (SBO 1KB),
             //           K step of 16 = two atoms = 2KB.
@@ -249,13 +255,13 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             UnitIter<BN> units(args, cluster, nclusters);
             Unit u;
             while (units.next(u)) {
-                const int buf = it & 1;
-                const uint32_t use = static_cast<uint32_t>(it >> 1);
+                const int buf = S::kAccBufs == 2 ? (it & 1) : 0;
+                const uint32_t use = static_cast<uint32_t>(S::kAccBufs == 2 ? (it >> 1) : it);
                 ++it;
                 const uint32_t idesc = idesc_base | (static_cast<uint32_t>(u.width >> 3) << 17);
                 mbar_wait_cluster(&tempty_bar[buf], (use & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * S::ACC_COLS);
                 for (int kb = u.k0; kb < u.k1; ++kb) {
                     mbar_wait(&full_bar[s], ph);
                     tc_fence_after();
@@ -263,9 +269,12 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     const uint32_t sb = sa + S::A_BYTES;
 #pragma unroll
                     for (int k = 0; k < S::BK / 16; ++k) {
-                        uint64_t ad = smem_desc_sw128(sa + k * a_kstep, a_lbo, 1024);
                         uint64_t bd = smem_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
-                        umma_f16<kCtaGroup>(d_tmem, ad, bd, idesc, (kb > u.k0 || k > 0) ? 1u : 0u);
+#pragma unroll
+                        for (int sl = 0; sl < kSlabs; ++sl) {  // slabs share the B operand
+                            uint64_t ad = smem_desc_sw128(sa + sl * S::SLAB_BYTES + k * a_kstep, a_lbo, 1024);
+                            umma_f16<kCtaGroup>(d_tmem + sl * BN, ad, bd, idesc, (kb > u.k0 || k > 0) ? 1u : 0u);
+                        }
                     }
                     if constexpr (kCtaGroup == 1) umma_commit(&empty_bar[s]);
                     else umma_commit_pair(&empty_bar[s], pair_mask);
@@ -322,8 +331,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             const bool last_unit = !have_next;
             int tm, tn;
             tile_coords(args, u.tile, tm, tn);
-            const int buf = it & 1;
-            const uint32_t use = static_cast<uint32_t>(it >> 1);
+            const int buf = S::kAccBufs == 2 ? (it & 1) : 0;
+            const uint32_t use = static_cast<uint32_t>(S::kAccBufs == 2 ? (it >> 1) : it);
             const uint32_t tile_use = static_cast<uint32_t>(it);
             ++it;
             mbar_wait(&tfull_bar[buf], use & 1);
@@ -331,7 +340,13 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             tc_fence_after();
             const int m = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM + row;
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                   static_cast<uint32_t>(buf * BN);
+                                   static_cast<uint32_t>(buf * S::ACC_COLS);
+            // whole-K units: chunk c of kSlabs * width/32 is slab c / nchu, columns
+            // (c % nchu) * 32 (TMEM columns c * 32: the slabs are adjacent)
+            const int nchu = u.width / 32;
+            const int nch_all = kSlabs * nchu;
+            auto chunk_row = [&](int c) { return (c / nchu) * S::BM_MMA; };
+            auto chunk_col = [&](int c) { return tn * BN + u.n_off + (c % nchu) * 32; };
             if constexpr (kSplitK == 1) {
                 auto release_tmem = [&] {
                     tc_fence_before();
@@ -342,14 +357,15 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     }
                     __syncwarp();
                 };
-                if (u.k0 == 0 && u.k1 == kb && args.c_tma && last_unit && args.ring_drain) {
+                if (u.k0 == 0 && u.k1 == kb && args.c_tma && last_unit && args.ring_drain &&
+                    nch_all * 32 * S::BM * 4 <= S::RING_BYTES) {
                     // the cluster's last unit: stage all chunks in the idle ring, TMA
                     // store them pairwise; TMEM loads double-buffered
                     const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
                     float* stage0 = reinterpret_cast<float*>(ring);
-                    drain_pairs(tbase, u.width / 32, [&](int c) { return stage0 + c * (32 * S::BM); },
+                    drain_pairs(tbase, nch_all, [&](int c) { return stage0 + c * (32 * S::BM); },
                                 [&](int c) {
-                                    tma_store_2d(&tmC, stage0 + c * (32 * S::BM), m_cta, tn * BN + u.n_off + c * 32);
+                                    tma_store_2d(&tmC, stage0 + c * (32 * S::BM), m_cta + chunk_row(c), chunk_col(c));
                                 });
                     release_tmem();
                 } else if (u.k0 == 0 && u.k1 == kb && args.c_tma) {
@@ -358,7 +374,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     // writes bank row % 32, conflict-free; one thread stores the chunk.
                     const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
 #pragma unroll 1
-                    for (int c = 0; c < u.width / 32; ++c) {
+                    for (int c = 0; c < nch_all; ++c) {
                         uint32_t r[32];
                         tmem_ld_32x32b_x32(tbase + c * 32, r);
                         float* stage = epi + (epi_chunk++ & 1) * (32 * S::BM);
@@ -370,7 +386,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                         fence_proxy_async();
                         epilogue_bar();
                         if (q == 0 && lane == 0) {
-                            tma_store_2d(&tmC, stage, m_cta, tn * BN + u.n_off + c * 32);
+                            tma_store_2d(&tmC, stage, m_cta + chunk_row(c), chunk_col(c));
                             bulk_commit_group();
                         }
                         __syncwarp();
@@ -379,16 +395,18 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 } else if (u.k0 == 0 && u.k1 == kb) {
                     // whole K range (a tile or an N-split half): TMEM -> RF -> GL
 #pragma unroll 1
-                    for (int c = 0; c < u.width / 32; ++c) {
+                    for (int c = 0; c < nch_all; ++c) {
                         uint32_t r[32];
                         tmem_ld_32x32b_x32(tbase + c * 32, r);
                         tmem_ld_wait();
                         float v[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                        store_row32_any(args, m, tn * BN + u.n_off + c * 32, v);
+                        store_row32_any(args, m + chunk_row(c), chunk_col(c), v);
                     }
                     release_tmem();
+                } else if (kSlabs > 1) {
+                    // slab tiles run whole-K units only (the planner never splits them)
                 } else if (args.sk_pull) {
                     // 2-slice pull fixup. Slice 1 (K-blocks [0, w)) publishes its whole
                     // partial; slice 0 ([w, kb)) streams it back chunk by chunk into
@@ -682,12 +700,12 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     }
 }
 
-template <int kCtaGroup, int BN, int kSplitK>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs>
 __global__ void __launch_bounds__(256, 1)
     fi_sm100_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
                   const __grid_constant__ GemmArgs args) {
-    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK>(tmA, tmB, tmB2, tmC, args);
+    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK, kSlabs>(tmA, tmB, tmB2, tmC, args);
 }
 
 }  // namespace fireiron::sm100

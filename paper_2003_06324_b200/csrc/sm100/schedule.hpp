@@ -63,13 +63,19 @@ struct GemmArgs {
     unsigned long long* trace = nullptr;
 };
 
-template <int kCtaGroup, int BN, int kSplitK>
+// kSlabs = 2 (CTA pairs, BN = 256 only): each CTA holds two 128-row A slabs and
+// the pair computes a 512 x 256 tile with two M = 256 MMAs per K step sharing
+// B -- 25% fewer operand bytes per FLOP than the 256 x 256 pair tile, at the
+// cost of the whole TMEM (2 x 256 columns): no accumulator double-buffering.
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1>
 struct GemmShape {
-    static constexpr int BM = 128;                 // rows per CTA (TMEM lanes)
-    static constexpr int BM_TILE = 128 * kCtaGroup;
+    static constexpr int BM = 128;                 // rows per CTA and slab (TMEM lanes)
+    static constexpr int BM_MMA = 128 * kCtaGroup; // rows of one MMA (a slab across the pair)
+    static constexpr int BM_TILE = BM_MMA * kSlabs;
     static constexpr int BK = 64;                  // one 128B swizzle span of 16-bit
     static constexpr int BN_LOCAL = BN / kCtaGroup;
-    static constexpr int A_BYTES = BM * BK * 2;
+    static constexpr int SLAB_BYTES = BM * BK * 2;
+    static constexpr int A_BYTES = SLAB_BYTES * kSlabs;
     static constexpr int B_BYTES = BN_LOCAL * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     // split-K reduction scratch: the fp32 partial tile (rows padded by 16B)
@@ -78,8 +84,10 @@ struct GemmShape {
     static constexpr int RED_BYTES = kSplitK > 1 ? BM * RED_LD * 4 : 0;
     static constexpr int kStages = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
     static_assert(kStages >= 2, "pipeline needs at least two stages");
-    static constexpr int kAccBufs = 2;
-    static constexpr int TMEM_COLS_RAW = kAccBufs * BN;
+    static constexpr int kAccBufs = kSlabs == 1 ? 2 : 1;
+    static constexpr int ACC_COLS = BN * kSlabs;   // TMEM columns of one accumulator buffer
+    static constexpr int TMEM_COLS_RAW = kAccBufs * ACC_COLS;
+    static_assert(TMEM_COLS_RAW <= 512, "accumulators exceed the 512 TMEM columns");
     static constexpr int TMEM_COLS = TMEM_COLS_RAW <= 32    ? 32
                                      : TMEM_COLS_RAW <= 64  ? 64
                                      : TMEM_COLS_RAW <= 128 ? 128

@@ -23,6 +23,7 @@ struct TcGemmConfig {
     int out_type = 0;    // 0 f32, 1 f16, 2 bf16
     int group_m = 8;     // raster band for the default tile order
     int stages = 0;      // pipeline depth (0 = deepest that fits in shared memory)
+    int slabs = 1;       // 2: A slabs per CTA (pair tile 512 x 256, cta_group 2, BN 256)
 };
 
 struct TcWorkspace;

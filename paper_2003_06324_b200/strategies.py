@@ -31,8 +31,11 @@ from __future__ import annotations
 
 def tc_strategy(m: int, n: int, k: int, *, ab: str = "f16", c: str = "f32", pair: bool = True,
                 tile_n: int = 256, split_k: int = 1, stages: int = 0,
-                layouts: tuple = ("colmajor", "colmajor", "colmajor"), swizzle: str = "") -> str:
-    bm = 256 if pair else 128
+                layouts: tuple = ("colmajor", "colmajor", "colmajor"), swizzle: str = "",
+                tile_m: int = 0) -> str:
+    """tile_m = 512 (with pair=True, tile_n=256): two A slabs per CTA, the pair
+    computes 512 x 256 with two M=256 MMAs per K step sharing B."""
+    bm = tile_m or (256 if pair else 128)
     head = f"spec MatMul({m},{n},{k})(GL,GL,GL)(Kernel) elems {ab} {ab} {c}"
     if tuple(layouts) != ("colmajor", "colmajor", "colmajor"):
         head += " layouts " + " ".join(layouts)
@@ -186,13 +189,21 @@ def c3_strategy() -> str:
 
 
 def c5_strategy(m: int = 16384, n: int = 16384, k: int = 16384) -> str:
-    """configs[4]: 16384^3 bf16 (per-GPU shard shape when sharded)."""
+    """configs[4]: 16384^3 bf16 (per-GPU shard shape when sharded). Shapes with
+    at least two waves of 512x256 pair tiles use the two-slab tile (25% fewer
+    operand bytes per FLOP: 16384^3 1580 vs 1460 TF, profiles/round1/
+    ab_slab_tile.log); smaller shards keep 256x256 pair tiles (more tiles than
+    clusters, double-buffered accumulators)."""
+    if m % 512 == 0 and n % 256 == 0 and (m // 512) * (n // 256) >= 148:
+        return tc_strategy(m, n, k, ab="bf16", pair=True, tile_n=256, tile_m=512)
     return tc_strategy(m, n, k, ab="bf16", pair=True, tile_n=256)
 
 
 def sweep_strategies(m: int, n: int, k: int, ab: str = "f16"):
     """Candidate tensor-core trees for one shape (config 4's shape sweep)."""
     out = {}
+    if m % 512 == 0 and n % 256 == 0 and k % 64 == 0 and (m // 512) * (n // 256) >= 74:
+        out["tc_pair_512x256"] = tc_strategy(m, n, k, ab=ab, pair=True, tile_n=256, tile_m=512)
     for pair in (True, False):
         bm = 256 if pair else 128
         for tn in (256, 128, 64):

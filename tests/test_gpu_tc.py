@@ -173,3 +173,36 @@ def test_forced_tail_modes(fi, oracle, monkeypatch, mode, layouts):
     # the last tiles (the tail) explicitly: a full 256-column strip at the end
     assert np.array_equal(c[-256:, -256:].astype(np.float64),
                           oracle.gemm_f64(ar[-256:], br[:, -256:]).astype(np.float64))
+
+
+@pytest.mark.parametrize("layouts", LAYOUTS, ids=lambda l: "".join(x[0] for x in l))
+@pytest.mark.parametrize("cout", ["f32", "f16"])
+def test_pair_512_slab_tile_integer_exact(fi, oracle, layouts, cout):
+    """tile 512 256 .pair: two A slabs per CTA, two M=256 MMAs per K step
+    sharing B, the whole TMEM per accumulator (whole-tile schedule)."""
+    m, n, k = 1024, 512, 320
+    s = fi.strategies.tc_strategy(m, n, k, layouts=layouts, c=cout, tile_m=512)
+    plan = fi.Plan(s)
+    assert plan.kind == "tcgen05" and plan.info.tile_m == 512 and plan.info.streamk == 0
+    a = oracle.fill(m, k, 21, True)
+    b = oracle.fill(k, n, 22, True)
+    want = oracle.gemm_f64(oracle.round_elem(a, "f16"), oracle.round_elem(b, "f16"))
+    got = plan.run_host(a, b)
+    assert np.array_equal(got, want if cout == "f32" else oracle.round_elem(want, "f16"))
+
+
+def test_pair_512_slab_tile_multi_wave_uniform(fi, oracle, monkeypatch):
+    # 4096 x 4096: 128 slab tiles over 74 clusters (two waves, the last one partial)
+    monkeypatch.setenv("FI_HOST_PIPELINE", "0")
+    m = n = 4096
+    k = 1024
+    s = fi.strategies.tc_strategy(m, n, k, tile_m=512)
+    c, ar, br = run(fi, oracle, s, m, n, k, False, seed=31)
+    rng = np.random.default_rng(3)
+    rows, cols = rng.integers(0, m, 4096), rng.integers(0, n, 4096)
+    want = oracle.sample_f64(ar, br, rows, cols)
+    got = c[rows, cols].astype(np.float64)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= TOL_NORMWISE
+    assert np.max(np.abs(got - want)) <= 1e-3
+    plain = fi.Plan(fi.strategies.tc_strategy(m, n, k))  # same products, 256x256 tiles
+    assert np.max(np.abs(plain.run_host(oracle.fill(m, k, 31, False), oracle.fill(k, n, 32, False)) - c)) <= 1e-4
