@@ -39,6 +39,7 @@ enum AsyncMutation : int {
     kMutSkipTmemEmptyWait = 4,      // the MMA reuses an accumulator before the epilogue drained it
     kMutRemainderSlotCollision = 5, // remainder partials all written to one workspace slot
     kMutUnpackedPeerStaging = 6,    // owners stage peers at j*nown chunks (the pre-remainder layout)
+    kMutTxUndercount = 7,           // expect_tx without the second B half of an N-half tile
 };
 
 struct AsyncCheckOptions {

@@ -21,6 +21,7 @@ CASES = {
     "c2_tcgen05": fi.strategies.c2_strategy,
     "c3_splitk": fi.strategies.c3_strategy,
     "pair512_slabs": lambda: fi.strategies.tc_strategy(8192, 8192, 8192, tile_m=512),
+    "pair_nhalves": lambda: fi.strategies.tc_strategy(8192, 8192, 8192, tile_n=512),
 }
 
 if __name__ == "__main__":

@@ -120,12 +120,12 @@ const char* role_name(int r) {
     return n[r];
 }
 
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1>
 class Checker {
-    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs>;
+    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
     static constexpr int kStages = S::kStages;
     static constexpr int NCH = BN / 32;
-    static constexpr int NCH_ALL = NCH * kSlabs;  // 32-column chunks of a tile's CTA rows, all slabs
+    static constexpr int NCH_ALL = NCH * kSlabs * kNHalves;  // 32-column chunks of a tile's CTA rows, all accumulators
     static constexpr int kChunkBytes = 32 * S::BM * 4;
     static constexpr int kGran = 1024;  // shared-memory cell granularity (bytes)
 
@@ -325,6 +325,10 @@ private:
     void complete_tx(Barrier& b, long bytes, const Clock& v) {
         join(b.pending, v);
         b.tx -= bytes;
+        if (b.tx < 0) {  // more bytes than the phase expected: they credit a later phase
+            ++rep_.deadlocks;
+            record("tx-mismatch", "barrier", -b.tx, "transaction bytes exceed expect_tx", "", -1);
+        }
         if (b.arrivals >= b.count && b.tx == 0) complete(b);
     }
     // try_wait.parity(p) succeeds once a phase of parity p completed after the
@@ -381,7 +385,11 @@ private:
             }
             ++it;
             const int b_rows = u.width / kCtaGroup;
-            const long bytes = S::A_BYTES + static_cast<long>(b_rows) * S::BK * 2;
+            // the kernel's expect_tx (per CTA of the pair) vs the bytes its loads deliver
+            const long expect = opt_.mutation == kMutTxUndercount
+                                    ? S::A_BYTES + static_cast<long>(b_rows) * S::BK * 2  // the first N-half kernel's bug
+                                    : S::stage_tx_bytes(b_rows) / kCtaGroup;
+            const long a_bytes = S::A_BYTES, b_bytes = static_cast<long>(b_rows) * S::BK * 2 * kNHalves;
             for (int kb = u.k0; kb < u.k1; ++kb) {
                 if (opt_.mutation != kMutSkipEmptyWait) {
                     co_await wait(C.empty[static_cast<size_t>(s)], ph ^ 1);
@@ -389,11 +397,14 @@ private:
                 }
                 ++vc_[static_cast<size_t>(P)][static_cast<size_t>(P)];
                 Barrier& full = C.full[static_cast<size_t>(s)];
-                expect_tx(full, bytes);
+                expect_tx(full, expect);
                 arrive(full, vc_[static_cast<size_t>(P)]);
                 issue(T, P);
-                smem(T, cta, kRing, static_cast<long>(s) * S::STAGE_BYTES, bytes, true);
-                complete_tx(full, bytes, vc_[static_cast<size_t>(T)]);
+                const long st = static_cast<long>(s) * S::STAGE_BYTES;
+                smem(T, cta, kRing, st, a_bytes, true);  // A slab(s)
+                complete_tx(full, a_bytes, vc_[static_cast<size_t>(T)]);
+                smem(T, cta, kRing, st + S::A_BYTES, b_bytes, true);  // B half (halves)
+                complete_tx(full, b_bytes, vc_[static_cast<size_t>(T)]);
                 if (++s == nst_) {
                     s = 0;
                     ph ^= 1;
@@ -419,14 +430,14 @@ private:
                 co_await wait(C.tempty[buf], (use & 1) ^ 1);
                 acquire(M, C.tempty[buf], (use & 1) ^ 1);
             }
-            const long bytes = S::A_BYTES + static_cast<long>(u.width / kCtaGroup) * S::BK * 2;
+            const long bytes = S::A_BYTES + static_cast<long>(u.width / kCtaGroup) * S::BK * 2 * kNHalves;
             for (int kb = u.k0; kb < u.k1; ++kb) {
                 co_await wait(C.full[static_cast<size_t>(s)], ph);
                 acquire(M, C.full[static_cast<size_t>(s)], ph);
                 ++vc_[static_cast<size_t>(M)][static_cast<size_t>(M)];
                 issue(X, M);
                 smem(X, cta, kRing, static_cast<long>(s) * S::STAGE_BYTES, bytes, false);
-                tmem(X, cta, buf, 0, u.width * kSlabs, true);
+                tmem(X, cta, buf, 0, u.width * kSlabs * kNHalves, true);
                 arrive(C.empty[static_cast<size_t>(s)], vc_[static_cast<size_t>(X)]);  // tcgen05.commit
                 if (++s == nst_) {
                     s = 0;
@@ -468,7 +479,7 @@ private:
             acquire(E, C.tfull[buf], use & 1);
             const int tile = u.tile;
             const int ch_off = u.n_off / 32;
-            const int nchu = u.width / 32, nch_all = nchu * kSlabs;
+            const int nchu = u.width / 32, nch_all = nchu * kSlabs * kNHalves;
             auto cchunk = [&](int c) { return (c / nchu) * NCH + ch_off + c % nchu; };  // C chunk id of TMEM chunk c
             auto release_tmem = [&] {
                 tick();
@@ -691,16 +702,16 @@ private:
     }
 };
 
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1>
 void run_checker(GemmArgs args, int sms, int force_slices, const AsyncCheckOptions& o, AsyncReport& rep) {
-    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs>;
+    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
     constexpr int kCluster = kCtaGroup * kSplitK;
     const int tiles = args.tiles_m * args.tiles_n;
     int clusters = sms / kCluster;
     if (o.max_active_clusters > 0 && o.max_active_clusters < clusters) clusters = o.max_active_clusters;
     // as the launcher: slab tiles (512-row pair tiles) run whole tiles only
     const SchedulePlan plan =
-        kSlabs > 1 ? plan_schedule<kCtaGroup, BN, kSplitK>(tiles, args.k_blocks, clusters, args.b_mn_major != 0, 0, 0,
+        kSlabs * kNHalves > 1 ? plan_schedule<kCtaGroup, BN, kSplitK>(tiles, args.k_blocks, clusters, args.b_mn_major != 0, 0, 0,
                                                            0, -1, 0)
                    : plan_schedule<kCtaGroup, BN, kSplitK>(tiles, args.k_blocks, clusters, args.b_mn_major != 0,
                                                            o.streamk, force_slices, o.remainder,
@@ -736,7 +747,7 @@ void run_checker(GemmArgs args, int sms, int force_slices, const AsyncCheckOptio
         Unit u;
         while (it.next(u)) ++rep.units;
     }
-    Checker<kCtaGroup, BN, kSplitK, kSlabs> chk(args, plan.clusters, plan.slots, o, rep);
+    Checker<kCtaGroup, BN, kSplitK, kSlabs, kNHalves> chk(args, plan.clusters, plan.slots, o, rep);
     chk.run();
 }
 
@@ -774,6 +785,10 @@ AsyncReport check_async(const Spec& root, const NodePtr& tree, const AsyncCheckO
     AsyncReport rep;
     if (tc.tile_m == 512) {
         run_checker<2, 256, 1, 2>(a, opts.num_sms, force_slices, opts, rep);
+        return rep;
+    }
+    if (tc.tile_n == 512) {
+        run_checker<2, 256, 1, 1, 2>(a, opts.num_sms, force_slices, opts, rep);
         return rep;
     }
 #define FI_CHECK(CG, BN_, SK)                                                        \

@@ -325,9 +325,11 @@ KernelSource generate(const Program& prog) {
           << "#include \"sm100/gemm_kernel.cuh\"\n\n"
           << "namespace fi_generated {\n"
           << "using namespace fireiron::sm100;\n"
-          << "constexpr int kCtaGroup = " << tc.cta_group << ", kTileN = " << tc.tile_n << ", kSplitK = " << tc.split_k
-          << ", kSlabs = " << tc.tile_m / (128 * tc.cta_group) << ";\n"
-          << "using Shape = GemmShape<kCtaGroup, kTileN, kSplitK, kSlabs>;\n"
+          << "constexpr int kCtaGroup = " << tc.cta_group << ", kMmaN = " << (tc.tile_n == 512 ? 256 : tc.tile_n)
+          << ", kSplitK = " << tc.split_k
+          << ", kSlabs = " << tc.tile_m / (128 * tc.cta_group) << ", kNHalves = " << (tc.tile_n == 512 ? 2 : 1)
+          << ";\n"
+          << "using Shape = GemmShape<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves>;\n"
           << "// grid: one persistent CTA per SM (clusters of kCtaGroup*kSplitK), "
           << "dynamic smem Shape::SMEM_BYTES\n"
           << "inline GemmArgs " << prog.entry_name << "_args(void* C) {\n"
@@ -348,7 +350,7 @@ KernelSource generate(const Program& prog) {
           << "(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,\n"
           << "    const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,\n"
           << "    const __grid_constant__ GemmArgs args) {\n"
-          << "  fi_sm100_gemm_body<kCtaGroup, kTileN, kSplitK, kSlabs>(tmA, tmB, tmB2, tmC, args);\n"
+          << "  fi_sm100_gemm_body<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves>(tmA, tmB, tmB2, tmC, args);\n"
           << "}\n"
           << "}  // namespace fi_generated\n";
         ks.source = o.str();
@@ -418,7 +420,8 @@ TcStrategy match_tc_strategy(const Spec& root, const NodePtr& tree, const MicroK
     // (two A slabs per CTA sharing B, the whole TMEM per accumulator)
     if (tc.tile_m != 128 * tc.cta_group && !(tc.cta_group == 2 && tc.tile_m == 512))
         return reject("block tile M must be 128, 256 with .pair, or 512 with .pair and N 256");
-    if (tc.tile_n != 64 && tc.tile_n != 128 && tc.tile_n != 256) return reject("block tile N must be 64, 128 or 256");
+    if (tc.tile_n != 64 && tc.tile_n != 128 && tc.tile_n != 256 && !(tc.tile_n == 512 && tc.cta_group == 2 && tc.tile_m == 256))
+        return reject("block tile N must be 64, 128 or 256 (512 with .pair and M 256: two N halves sharing A)");
     const DecompNode* nx = at(i++);
     if (nx && nx->kind == NodeKind::Split && nx->split_ref.splitk) {
         tc.split_k = static_cast<int>(root.k() / nx->split_k);
@@ -468,8 +471,8 @@ TcStrategy match_tc_strategy(const Spec& root, const NodePtr& tree, const MicroK
     } catch (const Error& e) {
         return reject(e.what());
     }
-    if (tc.tile_m == 512 && (tc.tile_n != 256 || tc.split_k > 1))
-        return reject("512-row pair tiles need N = 256 and no split-K (their accumulator fills TMEM)");
+    if ((tc.tile_m == 512 || tc.tile_n == 512) && (tc.tile_m * tc.tile_n != 512 * 256 || tc.split_k > 1))
+        return reject("512 x 256 / 256 x 512 pair tiles take no split-K (their accumulator fills TMEM)");
     if (tc.split_k > 1) {
         const int cluster = tc.split_k * tc.cta_group;
         if (cluster > 8 || (tc.split_k != 2 && tc.split_k != 4))

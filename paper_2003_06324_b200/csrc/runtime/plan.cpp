@@ -454,6 +454,8 @@ std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const 
         c.group_m = 8;
         c.stages = tc.stages;
         c.slabs = tc.tile_m / (128 * tc.cta_group);
+        c.n_halves = tc.tile_n == 512 ? 2 : 1;  // two N = 256 MMAs sharing A
+        c.bn = tc.tile_n / c.n_halves;
         if (sm100::tc_gemm_check(c, static_cast<int>(root.m()), static_cast<int>(root.n()),
                                  static_cast<int>(root.k())) != sm100::kTcOk)
             throw BackendError(103, "no tcgen05 kernel instance for this tile configuration");

@@ -57,10 +57,10 @@ TcWorkspace* shared_workspace() {
     return &ws;
 }
 
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1>
 int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream, bool dry_run = false) {
-    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs>;
-    auto kernel = fi_sm100_gemm<kCtaGroup, BN, kSplitK, kSlabs>;
+    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
+    auto kernel = fi_sm100_gemm<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
     constexpr int kCluster = kCtaGroup * kSplitK;
 
     const CUtensorMapDataType dt =
@@ -105,7 +105,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     args.N = p.N;
     args.K = p.K;
     args.tiles_m = p.M / S::BM_TILE;
-    args.tiles_n = p.N / BN;
+    args.tiles_n = p.N / S::BN_TILE;
     args.k_blocks = p.K / S::BK / kSplitK;
     args.ab_format = cfg.ab_format;
     args.a_mn_major = cfg.a_mn_major;
@@ -182,8 +182,8 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         const char* v = std::getenv("FI_TC_HEAD");
         return v ? std::atoi(v) : 1;
     }();
-    // slab tiles (512-row pair tiles) run whole tiles only: no tail split
-    const SchedulePlan plan = kSlabs > 1 ? plan_schedule<kCtaGroup, BN, kSplitK>(tiles, kb, clusters, cfg.b_mn_major != 0,
+    // slab / N-half tiles (512 x 256, 256 x 512 pair tiles) run whole tiles only: no tail split
+    const SchedulePlan plan = kSlabs * kNHalves > 1 ? plan_schedule<kCtaGroup, BN, kSplitK>(tiles, kb, clusters, cfg.b_mn_major != 0,
                                                                                 0, 0, 0, -1, 0)
                                          : plan_schedule<kCtaGroup, BN, kSplitK>(
                                                tiles, kb, clusters, cfg.b_mn_major != 0, p.streamk, p.force_slices,
@@ -269,14 +269,14 @@ TcLaunchInfo tc_gemm_last_launch() { return g_last; }
 
 int tc_gemm_stages(const TcGemmConfig& c) {
 #define FI_STAGES(CG, BN, SK)                                          \
-    if (c.cta_group == CG && c.bn == BN && c.split_k == SK && c.slabs == 1) { \
+    if (c.cta_group == CG && c.bn == BN && c.split_k == SK && c.slabs == 1 && c.n_halves == 1) { \
         const int mx = GemmShape<CG, BN, SK>::kStages;                 \
         return (c.stages > 0 && c.stages < mx) ? c.stages : mx;        \
     }
     FI_STAGES(1, 64, 1) FI_STAGES(1, 128, 1) FI_STAGES(1, 256, 1)
     FI_STAGES(2, 128, 1) FI_STAGES(2, 256, 1)
-    if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.slabs == 2) {
-        const int mx = GemmShape<2, 256, 1, 2>::kStages;
+    if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && (c.slabs == 2 || c.n_halves == 2)) {
+        const int mx = c.slabs == 2 ? GemmShape<2, 256, 1, 2>::kStages : GemmShape<2, 256, 1, 1, 2>::kStages;
         return (c.stages > 0 && c.stages < mx) ? c.stages : mx;
     }
     FI_STAGES(1, 64, 2) FI_STAGES(1, 128, 2) FI_STAGES(1, 128, 4) FI_STAGES(1, 256, 2) FI_STAGES(1, 256, 4) FI_STAGES(2, 256, 2) FI_STAGES(2, 256, 4) FI_STAGES(2, 128, 2) FI_STAGES(2, 128, 4)
@@ -286,8 +286,9 @@ int tc_gemm_stages(const TcGemmConfig& c) {
 
 int tc_gemm_smem_bytes(const TcGemmConfig& c) {
 #define FI_SMEM(CG, BN, SK) \
-    if (c.cta_group == CG && c.bn == BN && c.split_k == SK && c.slabs == 1) return GemmShape<CG, BN, SK>::SMEM_BYTES;
+    if (c.cta_group == CG && c.bn == BN && c.split_k == SK && c.slabs == 1 && c.n_halves == 1) return GemmShape<CG, BN, SK>::SMEM_BYTES;
     if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.slabs == 2) return GemmShape<2, 256, 1, 2>::SMEM_BYTES;
+    if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.n_halves == 2) return GemmShape<2, 256, 1, 1, 2>::SMEM_BYTES;
     FI_SMEM(1, 64, 1) FI_SMEM(1, 128, 1) FI_SMEM(1, 256, 1)
     FI_SMEM(2, 128, 1) FI_SMEM(2, 256, 1)
     FI_SMEM(1, 64, 2) FI_SMEM(1, 128, 2) FI_SMEM(1, 128, 4) FI_SMEM(1, 256, 2) FI_SMEM(1, 256, 4) FI_SMEM(2, 256, 2) FI_SMEM(2, 256, 4) FI_SMEM(2, 128, 2) FI_SMEM(2, 128, 4)
@@ -297,8 +298,9 @@ int tc_gemm_smem_bytes(const TcGemmConfig& c) {
 
 int tc_gemm_tmem_cols(const TcGemmConfig& c) {
 #define FI_TMEM(CG, BN, SK) \
-    if (c.cta_group == CG && c.bn == BN && c.split_k == SK && c.slabs == 1) return GemmShape<CG, BN, SK>::TMEM_COLS;
+    if (c.cta_group == CG && c.bn == BN && c.split_k == SK && c.slabs == 1 && c.n_halves == 1) return GemmShape<CG, BN, SK>::TMEM_COLS;
     if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.slabs == 2) return GemmShape<2, 256, 1, 2>::TMEM_COLS;
+    if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.n_halves == 2) return GemmShape<2, 256, 1, 1, 2>::TMEM_COLS;
     FI_TMEM(1, 64, 1) FI_TMEM(1, 128, 1) FI_TMEM(1, 256, 1)
     FI_TMEM(2, 128, 1) FI_TMEM(2, 256, 1)
     FI_TMEM(1, 64, 2) FI_TMEM(1, 128, 2) FI_TMEM(1, 128, 4) FI_TMEM(1, 256, 2) FI_TMEM(1, 256, 4) FI_TMEM(2, 256, 2) FI_TMEM(2, 256, 4) FI_TMEM(2, 128, 2) FI_TMEM(2, 128, 4)
@@ -308,10 +310,11 @@ int tc_gemm_tmem_cols(const TcGemmConfig& c) {
 
 int tc_gemm_check(const TcGemmConfig& c, int M, int N, int K) {
     if (!tc_gemm_stages(c)) return kTcErrUnsupported;
-    if (c.slabs != 1 && !(c.slabs == 2 && c.cta_group == 2 && c.bn == 256 && c.split_k == 1)) return kTcErrUnsupported;
+    const bool wide_ok = c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.slabs * c.n_halves == 2;
+    if (c.slabs * c.n_halves != 1 && !wide_ok) return kTcErrUnsupported;
     const int bm = 128 * c.cta_group * c.slabs;
     if (M <= 0 || N <= 0 || K <= 0) return kTcErrShape;
-    if (M % bm || N % c.bn || K % (64 * c.split_k)) return kTcErrShape;
+    if (M % bm || N % (c.bn * c.n_halves) || K % (64 * c.split_k)) return kTcErrShape;
     if (c.b_mn_major && (c.bn / c.cta_group) % 64) return kTcErrShape;
     if (c.split_k > 1 && (c.bn / c.split_k) % 32) return kTcErrShape;
     return kTcOk;
@@ -327,6 +330,7 @@ int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t
     int chk = tc_gemm_check(cfg, p.M, p.N, p.K);
     if (chk != kTcOk) return chk;
     if (cfg.slabs == 2) return launch_impl<2, 256, 1, 2>(cfg, p, stream, dry_run);
+    if (cfg.n_halves == 2) return launch_impl<2, 256, 1, 1, 2>(cfg, p, stream, dry_run);
 #define FI_LAUNCH(CG, BN, SK) \
     if (cfg.cta_group == CG && cfg.bn == BN && cfg.split_k == SK) return launch_impl<CG, BN, SK>(cfg, p, stream, dry_run);
     FI_LAUNCH(1, 64, 1) FI_LAUNCH(1, 128, 1) FI_LAUNCH(1, 256, 1)

@@ -102,12 +102,14 @@ __device__ __forceinline__ void epilogue_bar() { asm volatile("bar.sync 1, 128;"
 
 // Kernel body; the tensor maps must be __grid_constant__ kernel parameters
 // (TMA reads them through their parameter-space address).
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves>
 __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                                    const CUtensorMap& tmB2, const CUtensorMap& tmC,
                                                    const GemmArgs& args) {
-    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs>;
-    static_assert(kSlabs == 1 || (kCtaGroup == 2 && kSplitK == 1), "A slabs pair with CTA pairs, no cluster split-K");
+    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
+    static_assert(kSlabs * kNHalves == 1 || (kCtaGroup == 2 && kSplitK == 1 && kSlabs * kNHalves == 2),
+                  "slab / N-half tiles pair with CTA pairs, one doubling, no cluster split-K");
+    constexpr bool kWide = kSlabs * kNHalves > 1;  // whole-TMEM accumulator, whole-tile units only
     constexpr int kStages = S::kStages;
     constexpr int kClusterSize = kCtaGroup * kSplitK;
 
@@ -188,7 +190,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 tile_coords(args, u.tile, tm, tn);
                 const bool half = u.width != BN;
                 const int b_rows = u.width / kCtaGroup;  // B rows staged by this CTA
-                const uint32_t tx = static_cast<uint32_t>(S::A_BYTES + b_rows * S::BK * 2) * kCtaGroup;
+                const uint32_t tx = static_cast<uint32_t>(S::stage_tx_bytes(b_rows));
                 if constexpr (kSplitK > 1) {
                     // the ring doubles as the reduction scratch: wait until every
                     // peer has read my previous partial tile
@@ -198,7 +200,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 trace_stamp(args, it, 0);
                 ++it;
                 const int m0 = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
-                const int n0 = tn * BN + u.n_off + static_cast<int>(pair_rank) * b_rows;
+                const int n0 = tn * S::BN_TILE + u.n_off + static_cast<int>(pair_rank) * b_rows;
                 for (int kb = u.k0; kb < u.k1; ++kb) {
                     mbar_wait(&empty_bar[s], ph ^ 1);
                     uint8_t* sa = ring + s * S::STAGE_BYTES;
@@ -225,11 +227,16 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                             load(sas, &tmA, k0, m0s, pol_a);
                         }
                     }
-                    if (args.b_mn_major) {
-                        for (int j = 0; j < b_rows / 64; ++j)
-                            load(sb + j * 8192, &tmB, n0 + j * 64, k0, pol_b);
-                    } else {
-                        load(sb, half ? &tmB2 : &tmB, k0, n0, pol_b);  // tmB2: box of BN_LOCAL/2 rows
+#pragma unroll
+                    for (int h = 0; h < kNHalves; ++h) {  // N half h: rows n0 + h * BN
+                        uint8_t* sbh = sb + h * S::HALF_B_BYTES;
+                        const int n0h = n0 + h * BN;
+                        if (args.b_mn_major) {
+                            for (int j = 0; j < b_rows / 64; ++j)
+                                load(sbh + j * 8192, &tmB, n0h + j * 64, k0, pol_b);
+                        } else {
+                            load(sbh, half ? &tmB2 : &tmB, k0, n0h, pol_b);  // tmB2: box of BN_LOCAL/2 rows
+                        }
                     }
                     if (++s == nst) { s = 0; ph ^= 1; }
                 }
@@ -269,11 +276,22 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     const uint32_t sb = sa + S::A_BYTES;
 #pragma unroll
                     for (int k = 0; k < S::BK / 16; ++k) {
-                        uint64_t bd = smem_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
+                        const uint32_t acc = (kb > u.k0 || k > 0) ? 1u : 0u;
+                        if constexpr (kNHalves == 2) {
+                            // two N halves share A: the first MMA fills the A collector,
+                            // the second reuses it (A leaves shared memory once)
+                            uint64_t ad = smem_desc_sw128(sa + k * a_kstep, a_lbo, 1024);
+                            uint64_t bd0 = smem_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
+                            uint64_t bd1 = smem_desc_sw128(sb + S::HALF_B_BYTES + k * b_kstep, b_lbo, 1024);
+                            umma_f16_collect<kCtaGroup, 1>(d_tmem, ad, bd0, idesc, acc);
+                            umma_f16_collect<kCtaGroup, 2>(d_tmem + BN, ad, bd1, idesc, acc);
+                        } else {
+                            uint64_t bd = smem_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
 #pragma unroll
-                        for (int sl = 0; sl < kSlabs; ++sl) {  // slabs share the B operand
-                            uint64_t ad = smem_desc_sw128(sa + sl * S::SLAB_BYTES + k * a_kstep, a_lbo, 1024);
-                            umma_f16<kCtaGroup>(d_tmem + sl * BN, ad, bd, idesc, (kb > u.k0 || k > 0) ? 1u : 0u);
+                            for (int sl = 0; sl < kSlabs; ++sl) {  // slabs share the B operand
+                                uint64_t ad = smem_desc_sw128(sa + sl * S::SLAB_BYTES + k * a_kstep, a_lbo, 1024);
+                                umma_f16<kCtaGroup>(d_tmem + sl * BN, ad, bd, idesc, acc);
+                            }
                         }
                     }
                     if constexpr (kCtaGroup == 1) umma_commit(&empty_bar[s]);
@@ -341,12 +359,14 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             const int m = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM + row;
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                    static_cast<uint32_t>(buf * S::ACC_COLS);
-            // whole-K units: chunk c of kSlabs * width/32 is slab c / nchu, columns
-            // (c % nchu) * 32 (TMEM columns c * 32: the slabs are adjacent)
+            // whole-K units: TMEM chunk c (columns c * 32) of accumulator c / nchu --
+            // A slab (rows + slab * BM_MMA) or N half (columns + half * BN)
             const int nchu = u.width / 32;
-            const int nch_all = kSlabs * nchu;
-            auto chunk_row = [&](int c) { return (c / nchu) * S::BM_MMA; };
-            auto chunk_col = [&](int c) { return tn * BN + u.n_off + (c % nchu) * 32; };
+            const int nch_all = kSlabs * kNHalves * nchu;
+            auto chunk_row = [&](int c) { return kSlabs > 1 ? (c / nchu) * S::BM_MMA : 0; };
+            auto chunk_col = [&](int c) {
+                return tn * S::BN_TILE + u.n_off + (kNHalves > 1 ? (c / nchu) * BN : 0) + (c % nchu) * 32;
+            };
             if constexpr (kSplitK == 1) {
                 auto release_tmem = [&] {
                     tc_fence_before();
@@ -405,8 +425,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                         store_row32_any(args, m + chunk_row(c), chunk_col(c), v);
                     }
                     release_tmem();
-                } else if (kSlabs > 1) {
-                    // slab tiles run whole-K units only (the planner never splits them)
+                } else if (kWide) {
+                    // slab / N-half tiles run whole-K units only (the planner never splits them)
                 } else if (args.sk_pull) {
                     // 2-slice pull fixup. Slice 1 (K-blocks [0, w)) publishes its whole
                     // partial; slice 0 ([w, kb)) streams it back chunk by chunk into
@@ -700,12 +720,12 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     }
 }
 
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves>
 __global__ void __launch_bounds__(256, 1)
     fi_sm100_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
                   const __grid_constant__ GemmArgs args) {
-    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK, kSlabs>(tmA, tmB, tmB2, tmC, args);
+    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>(tmA, tmB, tmB2, tmC, args);
 }
 
 }  // namespace fireiron::sm100

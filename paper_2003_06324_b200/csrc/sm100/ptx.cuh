@@ -252,6 +252,27 @@ __device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64
     }
 }
 
+// Same with the A collector: kOp 1 = fill (read A, keep it), 2 = lastuse (reuse
+// the kept A, then release it) -- consecutive MMAs sharing A read it once.
+template <int kCtaGroup, int kOp>
+__device__ __forceinline__ void umma_f16_collect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                                 uint32_t idesc, uint32_t accumulate) {
+    static_assert(kCtaGroup == 2 && (kOp == 1 || kOp == 2), "pair MMAs with fill / lastuse");
+    if constexpr (kOp == 1) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+    }
+}
+
 // Arrive (once) on an mbarrier when all previously issued tcgen05 ops of this
 // thread complete. The 2-CTA form multicasts the arrive to the CTAs in mask.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {

@@ -67,16 +67,21 @@ struct GemmArgs {
 // the pair computes a 512 x 256 tile with two M = 256 MMAs per K step sharing
 // B -- 25% fewer operand bytes per FLOP than the 256 x 256 pair tile, at the
 // cost of the whole TMEM (2 x 256 columns): no accumulator double-buffering.
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1>
+// kNHalves = 2 (same restrictions): the pair computes 256 x 512 with two
+// N = 256 MMAs per K step sharing A through the tensor core's A collector
+// (read from shared memory once), the B stage holding both N halves.
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1>
 struct GemmShape {
     static constexpr int BM = 128;                 // rows per CTA and slab (TMEM lanes)
     static constexpr int BM_MMA = 128 * kCtaGroup; // rows of one MMA (a slab across the pair)
     static constexpr int BM_TILE = BM_MMA * kSlabs;
     static constexpr int BK = 64;                  // one 128B swizzle span of 16-bit
-    static constexpr int BN_LOCAL = BN / kCtaGroup;
+    static constexpr int BN_LOCAL = BN / kCtaGroup;  // B rows per CTA and MMA
+    static constexpr int BN_TILE = BN * kNHalves;
     static constexpr int SLAB_BYTES = BM * BK * 2;
     static constexpr int A_BYTES = SLAB_BYTES * kSlabs;
-    static constexpr int B_BYTES = BN_LOCAL * BK * 2;
+    static constexpr int HALF_B_BYTES = BN_LOCAL * BK * 2;
+    static constexpr int B_BYTES = HALF_B_BYTES * kNHalves;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     // split-K reduction scratch: the fp32 partial tile (rows padded by 16B)
     // reuses the operand ring once the tile's main loop has drained it
@@ -84,8 +89,8 @@ struct GemmShape {
     static constexpr int RED_BYTES = kSplitK > 1 ? BM * RED_LD * 4 : 0;
     static constexpr int kStages = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
     static_assert(kStages >= 2, "pipeline needs at least two stages");
-    static constexpr int kAccBufs = kSlabs == 1 ? 2 : 1;
-    static constexpr int ACC_COLS = BN * kSlabs;   // TMEM columns of one accumulator buffer
+    static constexpr int kAccBufs = kSlabs * kNHalves == 1 ? 2 : 1;
+    static constexpr int ACC_COLS = BN * kSlabs * kNHalves;  // TMEM columns of one accumulator buffer
     static constexpr int TMEM_COLS_RAW = kAccBufs * ACC_COLS;
     static_assert(TMEM_COLS_RAW <= 512, "accumulators exceed the 512 TMEM columns");
     static constexpr int TMEM_COLS = TMEM_COLS_RAW <= 32    ? 32
@@ -102,6 +107,9 @@ struct GemmShape {
     static constexpr int SMEM_BYTES = RING_BYTES + EPI_BYTES + BAR_BYTES + 1024;  // + align slack
     static_assert(SMEM_BYTES <= 227 * 1024, "exceeds the sm_100a per-CTA shared memory");
     static constexpr int kThreads = 256;
+    // transaction bytes one stage's TMA loads credit to the (leader's) full
+    // barrier: A slabs + B halves of b_rows rows, from every CTA of the pair
+    static constexpr FI_HD int stage_tx_bytes(int b_rows) { return (A_BYTES + b_rows * BK * 2 * kNHalves) * kCtaGroup; }
     static constexpr int WS_FLOATS = BN * BM;     // one CTA's partial tile
 };
 

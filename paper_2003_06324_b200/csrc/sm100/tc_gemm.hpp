@@ -24,6 +24,7 @@ struct TcGemmConfig {
     int group_m = 8;     // raster band for the default tile order
     int stages = 0;      // pipeline depth (0 = deepest that fits in shared memory)
     int slabs = 1;       // 2: A slabs per CTA (pair tile 512 x 256, cta_group 2, BN 256)
+    int n_halves = 1;    // 2: N halves sharing A (pair tile 256 x 512, cta_group 2, BN 256)
 };
 
 struct TcWorkspace;

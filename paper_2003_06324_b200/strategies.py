@@ -34,7 +34,8 @@ def tc_strategy(m: int, n: int, k: int, *, ab: str = "f16", c: str = "f32", pair
                 layouts: tuple = ("colmajor", "colmajor", "colmajor"), swizzle: str = "",
                 tile_m: int = 0) -> str:
     """tile_m = 512 (with pair=True, tile_n=256): two A slabs per CTA, the pair
-    computes 512 x 256 with two M=256 MMAs per K step sharing B."""
+    computes 512 x 256 with two M=256 MMAs per K step sharing B. tile_n = 512
+    (pair, tile_m 256): two N=256 MMAs per K step sharing A via the collector."""
     bm = tile_m or (256 if pair else 128)
     head = f"spec MatMul({m},{n},{k})(GL,GL,GL)(Kernel) elems {ab} {ab} {c}"
     if tuple(layouts) != ("colmajor", "colmajor", "colmajor"):
@@ -204,6 +205,8 @@ def sweep_strategies(m: int, n: int, k: int, ab: str = "f16"):
     out = {}
     if m % 512 == 0 and n % 256 == 0 and k % 64 == 0 and (m // 512) * (n // 256) >= 74:
         out["tc_pair_512x256"] = tc_strategy(m, n, k, ab=ab, pair=True, tile_n=256, tile_m=512)
+    if m % 256 == 0 and n % 512 == 0 and k % 64 == 0 and (m // 256) * (n // 512) >= 74:
+        out["tc_pair_256x512"] = tc_strategy(m, n, k, ab=ab, pair=True, tile_n=512)
     for pair in (True, False):
         bm = 256 if pair else 128
         for tn in (256, 128, 64):

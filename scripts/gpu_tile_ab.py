@@ -1,5 +1,5 @@
 """Interleaved A/B of block-tile strategies on large GEMMs (device time, L2
-flushed before every launch): 256x256 pair tile vs the 512x256 slab tile.
+flushed before every launch): 256x256 pair tile vs the 512x256 slab tile vs the 256x512 N-half tile.
 argv: m n k ab [rounds]"""
 import statistics, sys, time
 sys.path.insert(0, ".")
@@ -14,7 +14,8 @@ A = (torch.rand(k * m, device="cuda") - 0.5).to(dt); B = (torch.rand(n * k, devi
 C = torch.empty(m * n, device="cuda")
 flush = torch.empty(128 << 20, device="cuda"); s = torch.cuda.current_stream()
 plans = {"pair256x256": fi.Plan(fi.strategies.tc_strategy(m, n, k, ab=ab)),
-         "pair512x256": fi.Plan(fi.strategies.tc_strategy(m, n, k, ab=ab, tile_m=512))}
+         "pair512x256": fi.Plan(fi.strategies.tc_strategy(m, n, k, ab=ab, tile_m=512)),
+         "pair256x512": fi.Plan(fi.strategies.tc_strategy(m, n, k, ab=ab, tile_n=512))}
 for p in plans.values():
     for _ in range(3): p.launch(A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream)
 torch.cuda.synchronize()

@@ -63,6 +63,13 @@ def test_sweep_strategies_are_race_free(fi, m, n, k):
         assert r.ok, (name, r.text)
 
 
+@pytest.mark.parametrize("kw", [dict(tile_m=512), dict(tile_n=512)], ids=["slab512x256", "nhalf256x512"])
+@pytest.mark.parametrize("shape", [(1024, 512, 320), (4096, 4096, 1024), (8192, 8192, 2048)])
+def test_wide_pair_tiles_are_race_free(fi, tc, kw, shape):
+    r = fi.check_async(tc(*shape, **kw))
+    assert r.ok and r.mode == 0, r.text
+
+
 @pytest.mark.parametrize("stages", [2, 3, 4])
 def test_shallow_rings_are_race_free(fi, tc, stages):
     r = fi.check_async(tc(1024, 1024, 2048, stages=stages))
@@ -82,6 +89,7 @@ MUTANTS = [
     ("remainder_slot_collision", (1024, 1024, 32768), dict(split_k=4), "races"),
     ("unpacked_peer_staging", (768, 1024, 9600), {}, "capacity_errors"),  # 6 slices: staging past the ring
     ("skip_empty_wait", (1024, 1024, 4096), {}, "deadlocks"),             # parity runs ahead of the consumer
+    ("tx_undercount", (1024, 1024, 1024), dict(tile_n=512), "deadlocks"),  # N-half tile: B half 2 not expected
 ]
 
 

@@ -175,15 +175,20 @@ def test_forced_tail_modes(fi, oracle, monkeypatch, mode, layouts):
                           oracle.gemm_f64(ar[-256:], br[:, -256:]).astype(np.float64))
 
 
+WIDE = {"slab512x256": dict(tile_m=512), "nhalf256x512": dict(tile_n=512)}
+
+
+@pytest.mark.parametrize("wide", sorted(WIDE))
 @pytest.mark.parametrize("layouts", LAYOUTS, ids=lambda l: "".join(x[0] for x in l))
 @pytest.mark.parametrize("cout", ["f32", "f16"])
-def test_pair_512_slab_tile_integer_exact(fi, oracle, layouts, cout):
-    """tile 512 256 .pair: two A slabs per CTA, two M=256 MMAs per K step
-    sharing B, the whole TMEM per accumulator (whole-tile schedule)."""
+def test_wide_pair_tiles_integer_exact(fi, oracle, wide, layouts, cout):
+    """tile 512 256 .pair (two A slabs per CTA, two M=256 MMAs sharing B) and
+    tile 256 512 .pair (two N=256 MMAs sharing A through the A collector): the
+    whole TMEM per accumulator, whole-tile schedule."""
     m, n, k = 1024, 512, 320
-    s = fi.strategies.tc_strategy(m, n, k, layouts=layouts, c=cout, tile_m=512)
+    s = fi.strategies.tc_strategy(m, n, k, layouts=layouts, c=cout, **WIDE[wide])
     plan = fi.Plan(s)
-    assert plan.kind == "tcgen05" and plan.info.tile_m == 512 and plan.info.streamk == 0
+    assert plan.kind == "tcgen05" and plan.info.tile_m * plan.info.tile_n == 512 * 256 and plan.info.streamk == 0
     a = oracle.fill(m, k, 21, True)
     b = oracle.fill(k, n, 22, True)
     want = oracle.gemm_f64(oracle.round_elem(a, "f16"), oracle.round_elem(b, "f16"))
@@ -191,12 +196,13 @@ def test_pair_512_slab_tile_integer_exact(fi, oracle, layouts, cout):
     assert np.array_equal(got, want if cout == "f32" else oracle.round_elem(want, "f16"))
 
 
-def test_pair_512_slab_tile_multi_wave_uniform(fi, oracle, monkeypatch):
-    # 4096 x 4096: 128 slab tiles over 74 clusters (two waves, the last one partial)
+@pytest.mark.parametrize("wide", sorted(WIDE))
+def test_wide_pair_tiles_multi_wave_uniform(fi, oracle, monkeypatch, wide):
+    # 4096 x 4096: 128 wide tiles over 74 clusters (two waves, the last one partial)
     monkeypatch.setenv("FI_HOST_PIPELINE", "0")
     m = n = 4096
     k = 1024
-    s = fi.strategies.tc_strategy(m, n, k, tile_m=512)
+    s = fi.strategies.tc_strategy(m, n, k, **WIDE[wide])
     c, ar, br = run(fi, oracle, s, m, n, k, False, seed=31)
     rng = np.random.default_rng(3)
     rows, cols = rng.integers(0, m, 4096), rng.integers(0, n, 4096)
