@@ -163,10 +163,12 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         tma_prefetch_desc(&tmB2);
     }
     if (warp == 2) tmem_alloc<kCtaGroup>(tmem_slot, S::TMEM_COLS);
+    if (threadIdx.x == 64 && args.trace) args.trace[(blockIdx.x * 16 + 1) * 16 + 7] = global_timer_ns();  // alloc done
     tc_fence_before();
     if constexpr (kClusterSize > 1) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0 && args.trace) args.trace[(blockIdx.x * 16 + 2) * 16 + 7] = global_timer_ns();  // prologue synced
 
     const int nst = (args.stages > 0 && args.stages < kStages) ? args.stages : kStages;
     const int cluster = blockIdx.x / kClusterSize;
