@@ -139,6 +139,16 @@ int64_t fi_script_plan(const char* script_utf8, int64_t m, int64_t n, int64_t k,
  * matrix.hpp:67-80, for |x| < 65504). */
 fi_status fi_convert_f32(const float* src, void* dst, int64_t count, int elem, void* cuda_stream);
 
+/* Multi-GPU driver (one process per GPU): CUDA IPC export of a device buffer
+ * (handle of its allocation + the pointer's offset into it), import of a
+ * peer's buffer, and a stream-ordered copy (copy engines; over NVLink/NVSwitch
+ * between GPUs). Used to gather B chunks for configs[4] without NCCL kernels. */
+#define FI_IPC_HANDLE_BYTES 64
+fi_status fi_ipc_export(const void* dptr, void* handle_out, int64_t* offset_out);
+fi_status fi_ipc_open(const void* handle, int64_t offset, void** dptr_out);
+fi_status fi_ipc_close(void* dptr, int64_t offset);
+fi_status fi_copy_async(void* dst, const void* src, int64_t bytes, void* cuda_stream);
+
 /* Raw tensor-core GEMM entry (the kernel family behind FI_KIND_TCGEN05):
  * C = A*B, lda/ldb/ldc are physical leading dimensions in elements. */
 typedef struct fi_tc_config {

@@ -5,9 +5,11 @@ Partitioning (1-D over N): with g ranks, rank r owns
   A_r  = A[r*M/g:(r+1)*M/g, :]     (row shard, never communicated)
   B_r  = B[:, r*N/g:(r+1)*N/g]     (column shard, contiguous in col-major B)
 and computes the row band C_r = A_r * B (M/g x N). B is all-gathered over
-NVLink with NCCL as g per-owner broadcasts; the GEMM of column chunk j starts
-as soon as chunk j has arrived, so the collective overlaps the tensor-core
-work chunk by chunk (the own chunk needs no communication and runs first).
+NVLink, by default with copy-engine pulls from every peer's buffer mapped
+through CUDA IPC (PeerGather, no SM time), or with NCCL as g per-owner
+broadcasts (sharded_step); the GEMM of column chunk j starts as soon as chunk
+j has arrived, so the transfer overlaps the tensor-core work chunk by chunk
+(the own chunk needs no communication and runs first).
 
 Each chunk GEMM is the same tcgen05 strategy on the (M/g) x (N/g) x K shard
 shape; column chunks of col-major B and C are contiguous, so chunk j is a
@@ -84,3 +86,72 @@ def sharded_step(shard: Shard, a_local, b_local, b_full, c_local, gemm: Callable
         gemm(j, a_local, b_full[bo:bo + shard.b_chunk_elems],
              c_local[co:co + shard.m_local * shard.n_chunk])
     works[me].wait()
+
+
+class PeerGather:
+    """B all-gather over CUDA IPC and copy engines (the default transport of the
+    GPU driver): every rank exports its gathered-B buffer once, maps every
+    peer's buffer, and each step pulls the peers' chunks with DMA on one stream
+    per peer. The transfers use NVLink/NVSwitch copy engines and no SM time, so
+    they overlap the persistent tcgen05 GEMM, which keeps all SMs (NCCL's
+    broadcast kernels would take SMs from it). Chunk GEMM j waits only for the
+    event of chunk j."""
+
+    def __init__(self, shard: Shard, b_full, dist):
+        import ctypes as C
+        import torch
+        from . import _native as N
+        self.shard, self.N, self.C = shard, N, C
+        h = (C.c_char * 64)()
+        off = C.c_int64()
+        N.check(N.lib.fi_ipc_export(C.c_void_p(b_full.data_ptr()), h, C.byref(off)))
+        objs = [None] * shard.world
+        dist.all_gather_object(objs, (bytes(h), off.value))
+        self.peer = {}
+        for j, (hb, o) in enumerate(objs):
+            if j == shard.rank:
+                continue
+            p = C.c_void_p()
+            N.check(N.lib.fi_ipc_open(hb, o, C.byref(p)))
+            self.peer[j] = (p.value, o)
+        dev = b_full.device
+        self.streams = {j: torch.cuda.Stream(device=dev) for j in self.peer}
+        self.events = {j: torch.cuda.Event() for j in self.peer}
+        self.esize = b_full.element_size()
+
+    def pull(self, j: int, b_full):
+        """Issue the copy of owner j's chunk into b_full on j's stream; returns its event."""
+        import torch
+        p, _ = self.peer[j]
+        o = self.shard.b_chunk_offset(j) * self.esize
+        s = self.streams[j]
+        self.N.check(self.N.lib.fi_copy_async(self.C.c_void_p(b_full.data_ptr() + o), self.C.c_void_p(p + o),
+                                              self.shard.b_chunk_elems * self.esize, self.C.c_void_p(s.cuda_stream)))
+        self.events[j].record(s)
+        return self.events[j]
+
+    def close(self):
+        for p, o in self.peer.values():
+            self.N.lib.fi_ipc_close(self.C.c_void_p(p), o)
+        self.peer = {}
+
+
+def sharded_step_peer(shard: Shard, a_local, b_local, b_full, c_local, gemm: Callable, dist, pg: PeerGather):
+    """One step with copy-engine pulls: write my chunk into my gathered buffer,
+    synchronise (every owner's chunk in place, every peer done reading the
+    previous step's), pull the peers' chunks in rotated order and run each
+    chunk GEMM as soon as its chunk has landed."""
+    import torch
+    me = shard.rank
+    off = shard.b_chunk_offset(me)
+    b_full[off:off + shard.b_chunk_elems].copy_(b_local)
+    torch.cuda.current_stream().synchronize()
+    dist.barrier()
+    cur = torch.cuda.current_stream()
+    events = {j: pg.pull(j, b_full) for j in shard.order() if j != me}
+    for j in shard.order():
+        if j != me:
+            cur.wait_event(events[j])
+        bo, co = shard.b_chunk_offset(j), shard.c_chunk_offset(j)
+        gemm(j, a_local, b_full[bo:bo + shard.b_chunk_elems],
+             c_local[co:co + shard.m_local * shard.n_chunk])

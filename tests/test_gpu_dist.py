@@ -1,7 +1,10 @@
 """The M/N-sharded multi-GPU driver with the real tcgen05 kernels: two ranks
-share the one GPU of this environment over gloo (CUDA tensors), each computes
-its C row band with per-owner B chunk broadcasts overlapped with chunk GEMMs.
-Integer inputs: every rank's band must equal the fp64 oracle exactly."""
+share the one GPU of this environment (gloo for the process group), each
+computes its C row band with the B chunks gathered either by per-owner
+broadcasts or by copy-engine pulls from the peers' IPC-mapped buffers
+(PeerGather, the GPU driver's default), overlapped with chunk GEMMs. Integer
+inputs: every rank's band must equal the fp64 oracle exactly, two steps in a
+row (the second re-gathers into buffers the first step read)."""
 import os
 import socket
 import sys
@@ -20,14 +23,14 @@ def _port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, transport="broadcast"):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import torch
     import torch.distributed as dist
     import oracle
     import paper_2003_06324_b200 as fi
-    from paper_2003_06324_b200.dist import make_shard, sharded_step
+    from paper_2003_06324_b200.dist import PeerGather, make_shard, sharded_step, sharded_step_peer
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     m, n, k = 1024, 1024, 512
@@ -48,20 +51,32 @@ def _worker(rank, world, port, q):
     def gemm(j, aa, bb, cc):
         plan.launch(aa.data_ptr(), bb.data_ptr(), cc.data_ptr(), stream.cuda_stream)
 
-    sharded_step(sh, a_r, b_l, b_f, c_r, gemm, dist)
-    torch.cuda.synchronize()
-    band = c_r.cpu().numpy().reshape(n, sh.m_local).T
     want = oracle.gemm_f64(a[rank * sh.m_local:(rank + 1) * sh.m_local], b)
-    q.put((rank, bool(np.array_equal(band, want))))
+    ok = True
+    pg = PeerGather(sh, b_f, dist) if transport == "peer" else None
+    for _ in range(2):
+        c_r.fill_(float("nan"))
+        if pg is not None:
+            sharded_step_peer(sh, a_r, b_l, b_f, c_r, gemm, dist, pg)
+        else:
+            sharded_step(sh, a_r, b_l, b_f, c_r, gemm, dist)
+        torch.cuda.synchronize()
+        band = c_r.cpu().numpy().reshape(n, sh.m_local).T
+        ok = ok and bool(np.array_equal(band, want))
+    dist.barrier()
+    if pg is not None:
+        pg.close()
+    q.put((rank, ok))
     dist.destroy_process_group()
 
 
-def test_sharded_gemm_two_ranks_one_gpu():
+@pytest.mark.parametrize("transport", ["broadcast", "peer"])
+def test_sharded_gemm_two_ranks_one_gpu(transport):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, transport)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
