@@ -270,7 +270,7 @@ def ours_single(args, fi, torch):
 
 def ours_multi(args, fi, torch, rank, world):
     import torch.distributed as dist
-    from paper_2003_06324_b200.dist import PeerGather, make_shard, sharded_step, sharded_step_peer
+    from paper_2003_06324_b200.dist import PeerGather, make_shard, sharded_step, sharded_step_direct, sharded_step_peer
     wl = workload_of(args, world)
     m, n, k = wl["m"], wl["n"], wl["k"]
     shard = make_shard(m, n, k, world, rank)
@@ -289,13 +289,19 @@ def ours_multi(args, fi, torch, rank, world):
     def gemm(j, a, b, c):
         plan.launch(a.data_ptr(), b.data_ptr(), c.data_ptr(), stream.cuda_stream)
 
-    # B transport: copy-engine pulls from IPC-mapped peer buffers (default) or
-    # NCCL per-owner broadcasts (FI_DIST_TRANSPORT=nccl)
+    # B transport: copy-engine pulls from IPC-mapped peer buffers (default),
+    # NCCL per-owner broadcasts (FI_DIST_TRANSPORT=nccl), or direct TMA reads of
+    # the owners' buffers from inside the chunk GEMMs (FI_DIST_TRANSPORT=direct)
     transport = os.environ.get("FI_DIST_TRANSPORT", "peer")
-    pg = PeerGather(shard, Bf, dist) if transport == "peer" else None
+    pg = PeerGather(shard, Bf, dist) if transport in ("peer", "direct") else None
+
+    def gemm_ptr(j, a, bptr, c):
+        plan.launch(a.data_ptr(), bptr, c.data_ptr(), stream.cuda_stream)
 
     def step():
-        if pg is not None:
+        if transport == "direct":
+            sharded_step_direct(shard, A, Bl, Bf, C, gemm_ptr, dist, pg)
+        elif pg is not None:
             sharded_step_peer(shard, A, Bl, Bf, C, gemm, dist, pg)
         else:
             sharded_step(shard, A, Bl, Bf, C, gemm, dist)
@@ -328,8 +334,10 @@ def ours_multi(args, fi, torch, rank, world):
                 "vs_baseline": None, "dtype": wl["ab"] + " in / f32 acc", "data": "synthetic (uniform on device)",
                 "config": {"workload": wl["name"], "m": m, "n": n, "k": k, "parallelism": f"mn-shard{world}",
                            "shard": f"{shard.m_local}x{n} rows of C per GPU, B chunks of {shard.n_chunk} columns",
-                           "comm": ("copy-engine pulls of B chunks from IPC-mapped peer buffers" if pg is not None
-                                    else "NCCL per-owner broadcasts of B chunks") + ", overlapped with chunk GEMMs",
+                           "comm": {"peer": "copy-engine pulls of B chunks from IPC-mapped peer buffers, "
+                                            "overlapped with chunk GEMMs",
+                                    "direct": "chunk GEMMs read B over NVLink from the owners' IPC-mapped buffers",
+                                    }.get(transport, "NCCL per-owner broadcasts of B chunks, overlapped with chunk GEMMs"),
                            "percent_of_peak": 100.0 * value / (world * peaks["tflops"]),
                            "l2": "flushed before every timed step"},
                 "roofline": {"bound": "tensor", "achieved": value / world, "peak": peaks["tflops"], "unit": UNIT,

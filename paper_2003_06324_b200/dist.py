@@ -155,3 +155,20 @@ def sharded_step_peer(shard: Shard, a_local, b_local, b_full, c_local, gemm: Cal
         bo, co = shard.b_chunk_offset(j), shard.c_chunk_offset(j)
         gemm(j, a_local, b_full[bo:bo + shard.b_chunk_elems],
              c_local[co:co + shard.m_local * shard.n_chunk])
+
+
+def sharded_step_direct(shard: Shard, a_local, b_local, b_full, c_local, gemm_ptr: Callable, dist, pg: PeerGather):
+    """One step with no gather at all: chunk GEMM j's TMA descriptors point at
+    owner j's buffer through its IPC mapping, so B streams over NVLink tile by
+    tile inside the GEMM (the transfer fused into the kernel's loads).
+    gemm_ptr(j, a_local, b_ptr, c_chunk) launches chunk j on a raw B pointer."""
+    import torch
+    me = shard.rank
+    off = shard.b_chunk_offset(me)
+    b_full[off:off + shard.b_chunk_elems].copy_(b_local)
+    torch.cuda.current_stream().synchronize()
+    dist.barrier()
+    for j in shard.order():
+        bo, co = shard.b_chunk_offset(j), shard.c_chunk_offset(j)
+        ptr = b_full.data_ptr() + bo * pg.esize if j == me else pg.peer[j][0] + bo * pg.esize
+        gemm_ptr(j, a_local, ptr, c_local[co:co + shard.m_local * shard.n_chunk])

@@ -1,8 +1,9 @@
 """The M/N-sharded multi-GPU driver with the real tcgen05 kernels: two ranks
 share the one GPU of this environment (gloo for the process group), each
 computes its C row band with the B chunks gathered either by per-owner
-broadcasts or by copy-engine pulls from the peers' IPC-mapped buffers
-(PeerGather, the GPU driver's default), overlapped with chunk GEMMs. Integer
+broadcasts, by copy-engine pulls from the peers' IPC-mapped buffers
+(PeerGather, the GPU driver's default), or not at all (the chunk GEMM's TMA
+reads the owner's buffer through its IPC mapping), overlapped with chunk GEMMs. Integer
 inputs: every rank's band must equal the fp64 oracle exactly, two steps in a
 row (the second re-gathers into buffers the first step read)."""
 import os
@@ -30,7 +31,8 @@ def _worker(rank, world, port, q, transport="broadcast"):
     import torch.distributed as dist
     import oracle
     import paper_2003_06324_b200 as fi
-    from paper_2003_06324_b200.dist import PeerGather, make_shard, sharded_step, sharded_step_peer
+    from paper_2003_06324_b200.dist import (PeerGather, make_shard, sharded_step, sharded_step_direct,
+                                            sharded_step_peer)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     m, n, k = 1024, 1024, 512
@@ -53,10 +55,16 @@ def _worker(rank, world, port, q, transport="broadcast"):
 
     want = oracle.gemm_f64(a[rank * sh.m_local:(rank + 1) * sh.m_local], b)
     ok = True
-    pg = PeerGather(sh, b_f, dist) if transport == "peer" else None
+    pg = PeerGather(sh, b_f, dist) if transport in ("peer", "direct") else None
+
+    def gemm_ptr(j, aa, bptr, cc):
+        plan.launch(aa.data_ptr(), bptr, cc.data_ptr(), stream.cuda_stream)
+
     for _ in range(2):
         c_r.fill_(float("nan"))
-        if pg is not None:
+        if transport == "direct":
+            sharded_step_direct(sh, a_r, b_l, b_f, c_r, gemm_ptr, dist, pg)
+        elif pg is not None:
             sharded_step_peer(sh, a_r, b_l, b_f, c_r, gemm, dist, pg)
         else:
             sharded_step(sh, a_r, b_l, b_f, c_r, gemm, dist)
@@ -70,7 +78,7 @@ def _worker(rank, world, port, q, transport="broadcast"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("transport", ["broadcast", "peer"])
+@pytest.mark.parametrize("transport", ["broadcast", "peer", "direct"])
 def test_sharded_gemm_two_ranks_one_gpu(transport):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
