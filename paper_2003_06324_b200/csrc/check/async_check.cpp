@@ -796,7 +796,7 @@ AsyncReport check_async(const Spec& root, const NodePtr& tree, const AsyncCheckO
         run_checker<CG, BN_, SK>(a, opts.num_sms, force_slices, opts, rep);        \
         return rep;                                                                \
     }
-    FI_CHECK(1, 64, 1) FI_CHECK(1, 128, 1) FI_CHECK(1, 256, 1) FI_CHECK(2, 128, 1) FI_CHECK(2, 256, 1)
+    FI_CHECK(1, 64, 1) FI_CHECK(1, 128, 1) FI_CHECK(1, 256, 1) FI_CHECK(2, 64, 1) FI_CHECK(2, 128, 1) FI_CHECK(2, 256, 1)
     FI_CHECK(1, 64, 2) FI_CHECK(1, 128, 2) FI_CHECK(1, 128, 4) FI_CHECK(1, 256, 2) FI_CHECK(1, 256, 4)
     FI_CHECK(2, 256, 2) FI_CHECK(2, 256, 4) FI_CHECK(2, 128, 2) FI_CHECK(2, 128, 4)
 #undef FI_CHECK

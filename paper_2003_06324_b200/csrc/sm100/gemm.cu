@@ -274,7 +274,7 @@ int tc_gemm_stages(const TcGemmConfig& c) {
         return (c.stages > 0 && c.stages < mx) ? c.stages : mx;        \
     }
     FI_STAGES(1, 64, 1) FI_STAGES(1, 128, 1) FI_STAGES(1, 256, 1)
-    FI_STAGES(2, 128, 1) FI_STAGES(2, 256, 1)
+    FI_STAGES(2, 64, 1) FI_STAGES(2, 128, 1) FI_STAGES(2, 256, 1)
     if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && (c.slabs == 2 || c.n_halves == 2)) {
         const int mx = c.slabs == 2 ? GemmShape<2, 256, 1, 2>::kStages : GemmShape<2, 256, 1, 1, 2>::kStages;
         return (c.stages > 0 && c.stages < mx) ? c.stages : mx;
@@ -290,7 +290,7 @@ int tc_gemm_smem_bytes(const TcGemmConfig& c) {
     if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.slabs == 2) return GemmShape<2, 256, 1, 2>::SMEM_BYTES;
     if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.n_halves == 2) return GemmShape<2, 256, 1, 1, 2>::SMEM_BYTES;
     FI_SMEM(1, 64, 1) FI_SMEM(1, 128, 1) FI_SMEM(1, 256, 1)
-    FI_SMEM(2, 128, 1) FI_SMEM(2, 256, 1)
+    FI_SMEM(2, 64, 1) FI_SMEM(2, 128, 1) FI_SMEM(2, 256, 1)
     FI_SMEM(1, 64, 2) FI_SMEM(1, 128, 2) FI_SMEM(1, 128, 4) FI_SMEM(1, 256, 2) FI_SMEM(1, 256, 4) FI_SMEM(2, 256, 2) FI_SMEM(2, 256, 4) FI_SMEM(2, 128, 2) FI_SMEM(2, 128, 4)
 #undef FI_SMEM
     return 0;
@@ -302,7 +302,7 @@ int tc_gemm_tmem_cols(const TcGemmConfig& c) {
     if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.slabs == 2) return GemmShape<2, 256, 1, 2>::TMEM_COLS;
     if (c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.n_halves == 2) return GemmShape<2, 256, 1, 1, 2>::TMEM_COLS;
     FI_TMEM(1, 64, 1) FI_TMEM(1, 128, 1) FI_TMEM(1, 256, 1)
-    FI_TMEM(2, 128, 1) FI_TMEM(2, 256, 1)
+    FI_TMEM(2, 64, 1) FI_TMEM(2, 128, 1) FI_TMEM(2, 256, 1)
     FI_TMEM(1, 64, 2) FI_TMEM(1, 128, 2) FI_TMEM(1, 128, 4) FI_TMEM(1, 256, 2) FI_TMEM(1, 256, 4) FI_TMEM(2, 256, 2) FI_TMEM(2, 256, 4) FI_TMEM(2, 128, 2) FI_TMEM(2, 128, 4)
 #undef FI_TMEM
     return 0;
@@ -334,7 +334,7 @@ int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t
 #define FI_LAUNCH(CG, BN, SK) \
     if (cfg.cta_group == CG && cfg.bn == BN && cfg.split_k == SK) return launch_impl<CG, BN, SK>(cfg, p, stream, dry_run);
     FI_LAUNCH(1, 64, 1) FI_LAUNCH(1, 128, 1) FI_LAUNCH(1, 256, 1)
-    FI_LAUNCH(2, 128, 1) FI_LAUNCH(2, 256, 1)
+    FI_LAUNCH(2, 64, 1) FI_LAUNCH(2, 128, 1) FI_LAUNCH(2, 256, 1)
     FI_LAUNCH(1, 64, 2) FI_LAUNCH(1, 128, 2) FI_LAUNCH(1, 128, 4) FI_LAUNCH(1, 256, 2) FI_LAUNCH(1, 256, 4) FI_LAUNCH(2, 256, 2) FI_LAUNCH(2, 256, 4) FI_LAUNCH(2, 128, 2) FI_LAUNCH(2, 128, 4)
 #undef FI_LAUNCH
     return kTcErrUnsupported;

@@ -87,7 +87,8 @@ struct GemmShape {
     // reuses the operand ring once the tile's main loop has drained it
     static constexpr int RED_LD = BN + 4;
     static constexpr int RED_BYTES = kSplitK > 1 ? BM * RED_LD * 4 : 0;
-    static constexpr int kStages = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+    // as deep as 192 KiB allows, up to 12 stages (narrow tiles: short K-blocks need depth)
+    static constexpr int kStages = (192 * 1024) / STAGE_BYTES > 12 ? 12 : (192 * 1024) / STAGE_BYTES;
     static_assert(kStages >= 2, "pipeline needs at least two stages");
     static constexpr int kAccBufs = kSlabs * kNHalves == 1 ? 2 : 1;
     static constexpr int ACC_COLS = BN * kSlabs * kNHalves;  // TMEM columns of one accumulator buffer
@@ -99,7 +100,7 @@ struct GemmShape {
                                      : TMEM_COLS_RAW <= 256 ? 256
                                                             : 512;
     static constexpr int RING_BYTES = kStages * STAGE_BYTES;
-    static constexpr int BAR_BYTES = 256;
+    static constexpr int BAR_BYTES = 512;  // 2 * kStages + 8 mbarriers + the TMEM slot
     static_assert(RED_BYTES <= RING_BYTES, "split-K scratch must fit in the operand ring");
     // epilogue staging for TMA stores of C: two 32-column x 128-row fp32 chunks
     static constexpr int EPI_CHUNK_BYTES = 32 * BM * 4;

@@ -212,8 +212,8 @@ def sweep_strategies(m: int, n: int, k: int, ab: str = "f16"):
         for tn in (256, 128, 64):
             if m % bm or n % tn or k % 64:
                 continue
-            if pair and tn == 64:
-                continue
+            if pair and tn == 64 and n * m // (256 * 64) > 148:
+                continue  # pair 256x64: for narrow problems only
             name = f"tc_{'pair' if pair else 'cta'}_{bm}x{tn}"
             out[name] = tc_strategy(m, n, k, ab=ab, pair=pair, tile_n=tn)
             tiles = (m // bm) * (n // tn)

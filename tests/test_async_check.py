@@ -106,3 +106,10 @@ def test_non_tensor_core_tree_is_rejected(fi):
     from paper_2003_06324_b200 import FiError
     with pytest.raises(FiError):
         fi.check_async(fi.strategies.listing2(128, 128, 32))
+
+
+@pytest.mark.parametrize("shape", [(4096, 256, 4096), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 1024)])
+@pytest.mark.parametrize("mode", [-1, 1])
+def test_pair_256x64_schedules_are_race_free(fi, tc, shape, mode):
+    r = fi.check_async(tc(*shape, tile_n=64), streamk=mode)
+    assert r.ok, r.text

@@ -212,3 +212,16 @@ def test_wide_pair_tiles_multi_wave_uniform(fi, oracle, monkeypatch, wide):
     assert np.max(np.abs(got - want)) <= 1e-3
     plain = fi.Plan(fi.strategies.tc_strategy(m, n, k))  # same products, 256x256 tiles
     assert np.max(np.abs(plain.run_host(oracle.fill(m, k, 31, False), oracle.fill(k, n, 32, False)) - c)) <= 1e-4
+
+
+@pytest.mark.parametrize("layouts", LAYOUTS[:2], ids=lambda l: "".join(x[0] for x in l))
+@pytest.mark.parametrize("m,n,k", [(512, 256, 320), (4096, 256, 1024)])
+def test_pair_256x64_tile_integer_exact(fi, oracle, layouts, m, n, k):
+    """Narrow pair tile (cta_group::2, N = 64, 9-stage ring; K-major B only)."""
+    s = fi.strategies.tc_strategy(m, n, k, layouts=layouts, tile_n=64)
+    plan = fi.Plan(s)
+    assert plan.kind == "tcgen05" and plan.info.cta_group == 2 and plan.info.tile_n == 64
+    a = oracle.fill(m, k, 41, True)
+    b = oracle.fill(k, n, 42, True)
+    want = oracle.gemm_f64(oracle.round_elem(a, "f16"), oracle.round_elem(b, "f16"))
+    assert np.array_equal(plan.run_host(a, b), want)
