@@ -452,6 +452,7 @@ std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const 
         c.c_row_major = mm.c.layout.major == Major::RowMajor ? 1 : 0;
         c.out_type = elem_code(mm.c.elem);
         c.group_m = 8;
+        if (const char* e = std::getenv("FI_TC_GROUP_M")) c.group_m = std::atoi(e);  // raster band (experiments)
         c.stages = tc.stages;
         c.slabs = tc.tile_m / (128 * tc.cta_group);
         c.n_halves = tc.tile_n == 512 ? 2 : 1;  // two N = 256 MMAs sharing A
