@@ -40,6 +40,7 @@ enum AsyncMutation : int {
     kMutRemainderSlotCollision = 5, // remainder partials all written to one workspace slot
     kMutUnpackedPeerStaging = 6,    // owners stage peers at j*nown chunks (the pre-remainder layout)
     kMutTxUndercount = 7,           // expect_tx without the second B half of an N-half tile
+    kMutMcastSingleRelease = 8,     // multicast: a stage refilled after one pair's release, not both
 };
 
 struct AsyncCheckOptions {

@@ -84,6 +84,7 @@ struct TcStrategy {
     int cta_group = 1;     // .pair -> 2
     int tile_m = 128, tile_n = 128, tile_k = 64;
     int split_k = 1;       // .splitk ranks per output tile
+    int mcast = 1;         // .multicast: 2 pair units along N share A stages
     int stages = 0;        // .stages (0 = deepest that fits)
     std::vector<int32_t> tile_order;  // Block .swizzle/.layout schedule, empty = default raster
 };

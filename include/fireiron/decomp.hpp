@@ -3,6 +3,8 @@
 // the reference (proj/include/anvil/decomp.hpp:17-770); the sm_100a
 // refinements are additions:
 //   tile ... .to block .pair   -> the block unit is a CTA pair (tcgen05 cta_group::2)
+//   tile ... .to block .pair .multicast -> two neighbouring pair units (along N) form a
+//                                 cluster and receive each A stage by one TMA multicast
 //   split K .stages S          -> S-deep TMA/MMA mbarrier pipeline over the K loop
 //   split K .splitk            -> the split's chunks run in parallel on the CTAs
 //                                 of a cluster; the following epilog reduces the
@@ -32,6 +34,7 @@ struct TileRefinements {
     std::optional<Major> layout;  // unit id -> tile coordinate order
     Expr swizzle;                 // over the free variable "id"
     bool pair = false;            // sm_100a: block unit = CTA pair
+    bool multicast = false;       // sm_100a: two neighbouring block units along N share A by TMA multicast
 };
 
 struct LoadRefinements {

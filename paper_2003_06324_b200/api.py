@@ -63,7 +63,7 @@ def plan_summary(script: str, m: int = 0, n: int = 0, k: int = 0) -> str:
 
 MUTATIONS = {"none": 0, "skip_empty_wait": 1, "ring_drain_every_unit": 2, "flag_before_bulk_wait": 3,
              "skip_tmem_empty_wait": 4, "remainder_slot_collision": 5, "unpacked_peer_staging": 6,
-             "tx_undercount": 7}
+             "tx_undercount": 7, "mcast_single_release": 8}
 
 
 class AsyncReport:

@@ -120,8 +120,10 @@ const char* role_name(int r) {
     return n[r];
 }
 
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1, int kMcast = 1>
 class Checker {
+    // simulated CTAs per cluster: split-K ranks, or the two pairs of a multicast cluster
+    static constexpr int kRanks = kSplitK * kMcast;
     using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
     static constexpr int kStages = S::kStages;
     static constexpr int NCH = BN / 32;
@@ -132,7 +134,7 @@ class Checker {
 public:
     Checker(const GemmArgs& args, int clusters, long slots, const AsyncCheckOptions& o, AsyncReport& rep)
         : a_(args), ncl_(clusters), slots_(slots), opt_(o), rep_(rep) {
-        nctas_ = ncl_ * kSplitK;
+        nctas_ = ncl_ * kRanks;
         nagents_ = nctas_ * kRoles;
         vc_.assign(static_cast<size_t>(nagents_), Clock(static_cast<size_t>(nagents_), 0));
         ctas_.resize(static_cast<size_t>(nctas_));
@@ -143,7 +145,8 @@ public:
                             &c.pstage[0], &c.pstage[1]})
                 init_bar(*b, 1);
             for (auto& b : c.full) init_bar(b, 1);
-            for (auto& b : c.empty) init_bar(b, 1);
+            for (auto& b : c.empty)  // a release from every pair reading the slot
+                init_bar(b, opt_.mutation == kMutMcastSingleRelease ? 1 : kMcast);
             init_bar(c.tempty[0], 1);
             init_bar(c.tempty[1], 1);
             init_bar(c.rfull, kSplitK);
@@ -156,7 +159,7 @@ public:
     void run() {
         std::vector<Task> tasks;
         for (int c = 0; c < ncl_; ++c)
-            for (int r = 0; r < kSplitK; ++r) {
+            for (int r = 0; r < kRanks; ++r) {
                 tasks.push_back(producer(c, r));
                 tasks.push_back(mma(c, r));
                 tasks.push_back(epilogue(c, r));
@@ -188,7 +191,7 @@ public:
         }
         for (auto& t : tasks) t.h.destroy();
         // coverage: every 32-column chunk of every tile's CTA rows stored exactly once
-        const long tiles = static_cast<long>(a_.tiles_m) * a_.tiles_n;
+        const long tiles = static_cast<long>(a_.tiles_m) * a_.tiles_n * kMcast;  // per pair of a multicast unit
         for (long t = 0; t < tiles; ++t)
             for (int ch = 0; ch < NCH_ALL; ++ch) {
                 auto it = stores_.find(t * NCH_ALL + ch);
@@ -222,7 +225,7 @@ private:
     std::unordered_map<long, int> stores_;  // (tile*NCH_ALL + chunk) -> times stored
 
     int agent(int cta, int role) const { return cta * kRoles + role; }
-    int cta_of(int c, int r) const { return c * kSplitK + r; }
+    int cta_of(int c, int r) const { return c * kRanks + r; }
 
     void init_bar(Barrier& b, int count) {
         b.count = count;
@@ -322,13 +325,18 @@ private:
         std::fill(b.pending.begin(), b.pending.end(), 0);
     }
     void expect_tx(Barrier& b, long bytes) { b.tx += bytes; }
-    void complete_tx(Barrier& b, long bytes, const Clock& v) {
+    // phase = the barrier phase the issuer meant to credit. Bytes may arrive before
+    // that phase's expect_tx (the tx-count goes transiently negative, as on the
+    // hardware), but bytes for a phase that already completed spill into the next
+    // one: an expect_tx that under-counts its loads.
+    void complete_tx(Barrier& b, long bytes, const Clock& v, uint64_t phase = ~0ull) {
+        if (phase != ~0ull && phase < b.completed) {
+            ++rep_.deadlocks;
+            record("tx-mismatch", "barrier", static_cast<long>(bytes), "transaction bytes after their phase completed",
+                   "", -1);
+        }
         join(b.pending, v);
         b.tx -= bytes;
-        if (b.tx < 0) {  // more bytes than the phase expected: they credit a later phase
-            ++rep_.deadlocks;
-            record("tx-mismatch", "barrier", -b.tx, "transaction bytes exceed expect_tx", "", -1);
-        }
         if (b.arrivals >= b.count && b.tx == 0) complete(b);
     }
     // try_wait.parity(p) succeeds once a phase of parity p completed after the
@@ -375,6 +383,7 @@ private:
         Cta& C = ctas_[static_cast<size_t>(cta)];
         int s = 0;
         uint32_t ph = 0;
+        uint64_t lap = 0;  // ring wraps so far: the full-barrier phase this stage's loads credit
         int it = 0;
         UnitIter<BN> units(a_, cl, ncl_);
         Unit u;
@@ -401,13 +410,24 @@ private:
                 arrive(full, vc_[static_cast<size_t>(P)]);
                 issue(T, P);
                 const long st = static_cast<long>(s) * S::STAGE_BYTES;
-                smem(T, cta, kRing, st, a_bytes, true);  // A slab(s)
-                complete_tx(full, a_bytes, vc_[static_cast<size_t>(T)]);
+                if constexpr (kMcast > 1) {
+                    // my 64-row half of A, multicast to me and my rank-twin in the other pair
+                    for (int r2 = 0; r2 < kMcast; ++r2) {
+                        const int dst = cta_of(cl, r2);
+                        smem(T, dst, kRing, st + static_cast<long>(rank) * (a_bytes / 2), a_bytes / 2, true);
+                        complete_tx(ctas_[static_cast<size_t>(dst)].full[static_cast<size_t>(s)], a_bytes / 2,
+                                    vc_[static_cast<size_t>(T)], lap);
+                    }
+                } else {
+                    smem(T, cta, kRing, st, a_bytes, true);  // A slab(s)
+                    complete_tx(full, a_bytes, vc_[static_cast<size_t>(T)], lap);
+                }
                 smem(T, cta, kRing, st + S::A_BYTES, b_bytes, true);  // B half (halves)
-                complete_tx(full, b_bytes, vc_[static_cast<size_t>(T)]);
+                complete_tx(full, b_bytes, vc_[static_cast<size_t>(T)], lap);
                 if (++s == nst_) {
                     s = 0;
                     ph ^= 1;
+                    ++lap;
                 }
             }
         }
@@ -438,7 +458,13 @@ private:
                 issue(X, M);
                 smem(X, cta, kRing, static_cast<long>(s) * S::STAGE_BYTES, bytes, false);
                 tmem(X, cta, buf, 0, u.width * kSlabs * kNHalves, true);
-                arrive(C.empty[static_cast<size_t>(s)], vc_[static_cast<size_t>(X)]);  // tcgen05.commit
+                if constexpr (kMcast > 1) {  // commit multicast to every CTA of the cluster
+                    for (int r2 = 0; r2 < kMcast; ++r2)
+                        arrive(ctas_[static_cast<size_t>(cta_of(cl, r2))].empty[static_cast<size_t>(s)],
+                               vc_[static_cast<size_t>(X)]);
+                } else {
+                    arrive(C.empty[static_cast<size_t>(s)], vc_[static_cast<size_t>(X)]);  // tcgen05.commit
+                }
                 if (++s == nst_) {
                     s = 0;
                     ph ^= 1;
@@ -477,7 +503,7 @@ private:
             ++it;
             co_await wait(C.tfull[buf], use & 1);
             acquire(E, C.tfull[buf], use & 1);
-            const int tile = u.tile;
+            const int tile = u.tile * kMcast + (kMcast > 1 ? rank : 0);  // a multicast unit = two pair tiles
             const int ch_off = u.n_off / 32;
             const int nchu = u.width / 32, nch_all = nchu * kSlabs * kNHalves;
             auto cchunk = [&](int c) { return (c / nchu) * NCH + ch_off + c % nchu; };  // C chunk id of TMEM chunk c
@@ -702,16 +728,16 @@ private:
     }
 };
 
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1, int kMcast = 1>
 void run_checker(GemmArgs args, int sms, int force_slices, const AsyncCheckOptions& o, AsyncReport& rep) {
     using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
-    constexpr int kCluster = kCtaGroup * kSplitK;
+    constexpr int kCluster = kCtaGroup * kSplitK * kMcast;
     const int tiles = args.tiles_m * args.tiles_n;
     int clusters = sms / kCluster;
     if (o.max_active_clusters > 0 && o.max_active_clusters < clusters) clusters = o.max_active_clusters;
     // as the launcher: slab tiles (512-row pair tiles) run whole tiles only
     const SchedulePlan plan =
-        kSlabs * kNHalves > 1 ? plan_schedule<kCtaGroup, BN, kSplitK>(tiles, args.k_blocks, clusters, args.b_mn_major != 0, 0, 0,
+        kSlabs * kNHalves * kMcast > 1 ? plan_schedule<kCtaGroup, BN, kSplitK>(tiles, args.k_blocks, clusters, args.b_mn_major != 0, 0, 0,
                                                            0, -1, 0)
                    : plan_schedule<kCtaGroup, BN, kSplitK>(tiles, args.k_blocks, clusters, args.b_mn_major != 0,
                                                            o.streamk, force_slices, o.remainder,
@@ -747,7 +773,7 @@ void run_checker(GemmArgs args, int sms, int force_slices, const AsyncCheckOptio
         Unit u;
         while (it.next(u)) ++rep.units;
     }
-    Checker<kCtaGroup, BN, kSplitK, kSlabs, kNHalves> chk(args, plan.clusters, plan.slots, o, rep);
+    Checker<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kMcast> chk(args, plan.clusters, plan.slots, o, rep);
     chk.run();
 }
 
@@ -774,7 +800,7 @@ AsyncReport check_async(const Spec& root, const NodePtr& tree, const AsyncCheckO
     a.N = static_cast<int>(N);
     a.K = static_cast<int>(K);
     a.tiles_m = static_cast<int>(M / bm);
-    a.tiles_n = static_cast<int>(N / tc.tile_n);
+    a.tiles_n = static_cast<int>(N / (tc.tile_n * tc.mcast));
     a.k_blocks = static_cast<int>(K / 64 / split_k);
     a.b_mn_major = mm.b.layout.major == Major::RowMajor ? 1 : 0;
     a.c_row_major = mm.c.layout.major == Major::RowMajor ? 1 : 0;
@@ -789,6 +815,12 @@ AsyncReport check_async(const Spec& root, const NodePtr& tree, const AsyncCheckO
     }
     if (tc.tile_n == 512) {
         run_checker<2, 256, 1, 1, 2>(a, opts.num_sms, force_slices, opts, rep);
+        return rep;
+    }
+    if (tc.mcast == 2) {
+        if (tc.tile_n == 64) run_checker<2, 64, 1, 1, 1, 2>(a, opts.num_sms, force_slices, opts, rep);
+        else if (tc.tile_n == 128) run_checker<2, 128, 1, 1, 1, 2>(a, opts.num_sms, force_slices, opts, rep);
+        else run_checker<2, 256, 1, 1, 1, 2>(a, opts.num_sms, force_slices, opts, rep);
         return rep;
     }
 #define FI_CHECK(CG, BN_, SK)                                                        \

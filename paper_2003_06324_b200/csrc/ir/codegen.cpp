@@ -328,7 +328,7 @@ KernelSource generate(const Program& prog) {
           << "constexpr int kCtaGroup = " << tc.cta_group << ", kMmaN = " << (tc.tile_n == 512 ? 256 : tc.tile_n)
           << ", kSplitK = " << tc.split_k
           << ", kSlabs = " << tc.tile_m / (128 * tc.cta_group) << ", kNHalves = " << (tc.tile_n == 512 ? 2 : 1)
-          << ";\n"
+          << ", kMcast = " << tc.mcast << ";\n"
           << "using Shape = GemmShape<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves>;\n"
           << "// grid: one persistent CTA per SM (clusters of kCtaGroup*kSplitK), "
           << "dynamic smem Shape::SMEM_BYTES\n"
@@ -337,7 +337,8 @@ KernelSource generate(const Program& prog) {
           << "  a.C = C;\n"
           << "  a.M = " << prog.root.m() << "; a.N = " << prog.root.n() << "; a.K = " << prog.root.k() << ";\n"
           << "  a.ldc = " << mm.c.layout.leading_dim(mm.c.rows, mm.c.cols) << ";\n"
-          << "  a.tiles_m = " << prog.root.m() / tc.tile_m << "; a.tiles_n = " << prog.root.n() / tc.tile_n << ";\n"
+          << "  a.tiles_m = " << prog.root.m() / tc.tile_m << "; a.tiles_n = " << prog.root.n() / (tc.tile_n * tc.mcast)
+          << ";\n"
           << "  a.k_blocks = " << prog.root.k() / tc.tile_k / tc.split_k << ";\n"
           << "  a.ab_format = " << (mm.a.elem == ElemType::BF16 ? 1 : 0) << ";  // " << elem_name(mm.a.elem) << "\n"
           << "  a.a_mn_major = " << (mm.a.layout.major == Major::ColMajor ? 1 : 0) << ";\n"
@@ -350,7 +351,7 @@ KernelSource generate(const Program& prog) {
           << "(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,\n"
           << "    const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,\n"
           << "    const __grid_constant__ GemmArgs args) {\n"
-          << "  fi_sm100_gemm_body<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves>(tmA, tmB, tmB2, tmC, args);\n"
+          << "  fi_sm100_gemm_body<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves, kMcast>(tmA, tmB, tmB2, tmC, args);\n"
           << "}\n"
           << "}  // namespace fi_generated\n";
         ks.source = o.str();
@@ -414,6 +415,7 @@ TcStrategy match_tc_strategy(const Spec& root, const NodePtr& tree, const MicroK
     if (!blk || blk->kind != NodeKind::Tile || !blk->tile_ref.to || *blk->tile_ref.to != ComputeLevel::Block)
         return reject("first step must be the block tile (.to block)");
     tc.cta_group = blk->tile_ref.pair ? 2 : 1;
+    tc.mcast = blk->tile_ref.multicast ? 2 : 1;
     tc.tile_m = static_cast<int>(blk->tile_r);
     tc.tile_n = static_cast<int>(blk->tile_c);
     // one TMEM lane per row: 128, 256 with .pair, or 512 with .pair and N = 256
@@ -471,6 +473,8 @@ TcStrategy match_tc_strategy(const Spec& root, const NodePtr& tree, const MicroK
     } catch (const Error& e) {
         return reject(e.what());
     }
+    if (tc.mcast > 1 && (tc.tile_m != 256 || tc.tile_n > 256 || tc.split_k > 1 || root.n() % (2L * tc.tile_n)))
+        return reject("multicast pairs need 256-row tiles of N <= 256, no split-K, and N a multiple of 2 tiles");
     if ((tc.tile_m == 512 || tc.tile_n == 512) && (tc.tile_m * tc.tile_n != 512 * 256 || tc.split_k > 1))
         return reject("512 x 256 / 256 x 512 pair tiles take no split-K (their accumulator fills TMEM)");
     if (tc.split_k > 1) {

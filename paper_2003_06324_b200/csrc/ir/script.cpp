@@ -303,6 +303,9 @@ NodePtr parse_step(Cursor& cur, const Line& ln, NodePtr prev) {
             } else if (k == ".pair") {
                 ref.pair = true;
                 ++i;
+            } else if (k == ".multicast") {
+                ref.multicast = true;
+                ++i;
             } else {
                 parse_fail(ln.number, t[i].col, "unknown tile refinement '" + t[i].text + "'");
             }
@@ -598,6 +601,7 @@ void print_chain(const NodePtr& node, std::string& out, int indent) {
                 if (n->tile_ref.layout) l += " .layout " + major_tok(*n->tile_ref.layout);
                 if (n->tile_ref.swizzle) l += " .swizzle " + expr_token(n->tile_ref.swizzle);
                 if (n->tile_ref.pair) l += " .pair";
+                if (n->tile_ref.multicast) l += " .multicast";
                 if (n->tile_ref.unroll) l += " .unroll";
                 out += l + "\n";
                 break;

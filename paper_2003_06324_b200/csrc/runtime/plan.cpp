@@ -456,6 +456,7 @@ std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const 
         c.stages = tc.stages;
         c.slabs = tc.tile_m / (128 * tc.cta_group);
         c.n_halves = tc.tile_n == 512 ? 2 : 1;  // two N = 256 MMAs sharing A
+        c.mcast = tc.mcast;
         c.bn = tc.tile_n / c.n_halves;
         if (sm100::tc_gemm_check(c, static_cast<int>(root.m()), static_cast<int>(root.n()),
                                  static_cast<int>(root.k())) != sm100::kTcOk)
@@ -493,7 +494,7 @@ std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const 
         info.tile_m = tc.tile_m;
         info.tile_n = tc.tile_n;
         info.split_k = tc.split_k;
-        info.cluster = tc.cta_group * c.split_k;
+        info.cluster = tc.cta_group * c.split_k * c.mcast;
         info.stages = sm100::tc_gemm_stages(c);
         info.tmem_cols = sm100::tc_gemm_tmem_cols(c);
         info.shared_bytes = sm100::tc_gemm_smem_bytes(c);

@@ -57,11 +57,11 @@ TcWorkspace* shared_workspace() {
     return &ws;
 }
 
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1, int kMcast = 1>
 int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream, bool dry_run = false) {
     using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
-    auto kernel = fi_sm100_gemm<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
-    constexpr int kCluster = kCtaGroup * kSplitK;
+    auto kernel = fi_sm100_gemm<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kMcast>;
+    constexpr int kCluster = kCtaGroup * kSplitK * kMcast;
 
     const CUtensorMapDataType dt =
         cfg.ab_format == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
@@ -70,7 +70,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     if (cfg.a_mn_major)
         r = encode_2d(&tmA, dt, p.A, p.M, p.K, static_cast<uint64_t>(p.lda) * 2, 64, 64);
     else
-        r = encode_2d(&tmA, dt, p.A, p.K, p.M, static_cast<uint64_t>(p.lda) * 2, 64, S::BM);
+        r = encode_2d(&tmA, dt, p.A, p.K, p.M, static_cast<uint64_t>(p.lda) * 2, 64, kMcast > 1 ? 64 : S::BM);
     if (r != CUDA_SUCCESS) return kTcErrTensorMap;
     if (cfg.b_mn_major)
         r = encode_2d(&tmB, dt, p.B, p.N, p.K, static_cast<uint64_t>(p.ldb) * 2, 64, 64);
@@ -105,7 +105,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     args.N = p.N;
     args.K = p.K;
     args.tiles_m = p.M / S::BM_TILE;
-    args.tiles_n = p.N / S::BN_TILE;
+    args.tiles_n = p.N / (S::BN_TILE * kMcast);  // scheduled units span both pairs of a multicast cluster
     args.k_blocks = p.K / S::BK / kSplitK;
     args.ab_format = cfg.ab_format;
     args.a_mn_major = cfg.a_mn_major;
@@ -183,7 +183,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         return v ? std::atoi(v) : 1;
     }();
     // slab / N-half tiles (512 x 256, 256 x 512 pair tiles) run whole tiles only: no tail split
-    const SchedulePlan plan = kSlabs * kNHalves > 1 ? plan_schedule<kCtaGroup, BN, kSplitK>(tiles, kb, clusters, cfg.b_mn_major != 0,
+    const SchedulePlan plan = kSlabs * kNHalves * kMcast > 1 ? plan_schedule<kCtaGroup, BN, kSplitK>(tiles, kb, clusters, cfg.b_mn_major != 0,
                                                                                 0, 0, 0, -1, 0)
                                          : plan_schedule<kCtaGroup, BN, kSplitK>(
                                                tiles, kb, clusters, cfg.b_mn_major != 0, p.streamk, p.force_slices,
@@ -312,9 +312,11 @@ int tc_gemm_check(const TcGemmConfig& c, int M, int N, int K) {
     if (!tc_gemm_stages(c)) return kTcErrUnsupported;
     const bool wide_ok = c.cta_group == 2 && c.bn == 256 && c.split_k == 1 && c.slabs * c.n_halves == 2;
     if (c.slabs * c.n_halves != 1 && !wide_ok) return kTcErrUnsupported;
+    if (c.mcast != 1 && !(c.mcast == 2 && c.cta_group == 2 && c.split_k == 1 && c.slabs * c.n_halves == 1))
+        return kTcErrUnsupported;
     const int bm = 128 * c.cta_group * c.slabs;
     if (M <= 0 || N <= 0 || K <= 0) return kTcErrShape;
-    if (M % bm || N % (c.bn * c.n_halves) || K % (64 * c.split_k)) return kTcErrShape;
+    if (M % bm || N % (c.bn * c.n_halves * c.mcast) || K % (64 * c.split_k)) return kTcErrShape;
     if (c.b_mn_major && (c.bn / c.cta_group) % 64) return kTcErrShape;
     if (c.split_k > 1 && (c.bn / c.split_k) % 32) return kTcErrShape;
     return kTcOk;
@@ -331,6 +333,12 @@ int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t
     if (chk != kTcOk) return chk;
     if (cfg.slabs == 2) return launch_impl<2, 256, 1, 2>(cfg, p, stream, dry_run);
     if (cfg.n_halves == 2) return launch_impl<2, 256, 1, 1, 2>(cfg, p, stream, dry_run);
+    if (cfg.mcast == 2) {
+        if (cfg.bn == 64) return launch_impl<2, 64, 1, 1, 1, 2>(cfg, p, stream, dry_run);
+        if (cfg.bn == 128) return launch_impl<2, 128, 1, 1, 1, 2>(cfg, p, stream, dry_run);
+        if (cfg.bn == 256) return launch_impl<2, 256, 1, 1, 1, 2>(cfg, p, stream, dry_run);
+        return kTcErrUnsupported;
+    }
 #define FI_LAUNCH(CG, BN, SK) \
     if (cfg.cta_group == CG && cfg.bn == BN && cfg.split_k == SK) return launch_impl<CG, BN, SK>(cfg, p, stream, dry_run);
     FI_LAUNCH(1, 64, 1) FI_LAUNCH(1, 128, 1) FI_LAUNCH(1, 256, 1)

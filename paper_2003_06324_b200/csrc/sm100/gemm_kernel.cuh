@@ -102,7 +102,7 @@ __device__ __forceinline__ void epilogue_bar() { asm volatile("bar.sync 1, 128;"
 
 // Kernel body; the tensor maps must be __grid_constant__ kernel parameters
 // (TMA reads them through their parameter-space address).
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves, int kMcast>
 __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                                    const CUtensorMap& tmB2, const CUtensorMap& tmC,
                                                    const GemmArgs& args) {
@@ -110,8 +110,14 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     static_assert(kSlabs * kNHalves == 1 || (kCtaGroup == 2 && kSplitK == 1 && kSlabs * kNHalves == 2),
                   "slab / N-half tiles pair with CTA pairs, one doubling, no cluster split-K");
     constexpr bool kWide = kSlabs * kNHalves > 1;  // whole-TMEM accumulator, whole-tile units only
+    // kMcast = 2 (.multicast): a cluster of two CTA pairs computes two tiles that are
+    // neighbours along N; each pair's CTA of rank r receives the same A rows, so
+    // the two CTAs of rank r load one 64-row half each and multicast it to both.
+    // A stage slot is refilled only after both pairs' MMAs released it.
+    static_assert(kMcast == 1 || (kCtaGroup == 2 && kSplitK == 1 && !kWide), "multicast pairs tiles of one CTA pair");
+    constexpr int kBNTile = S::BN_TILE * kMcast;  // columns of one scheduled unit (both pairs)
     constexpr int kStages = S::kStages;
-    constexpr int kClusterSize = kCtaGroup * kSplitK;
+    constexpr int kClusterSize = kCtaGroup * kSplitK * kMcast;
 
     extern __shared__ uint8_t smem_raw[];
     // 1024B alignment for the 128B-swizzle atoms
@@ -134,9 +140,12 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     const int lane = threadIdx.x % 32;
     const uint32_t crank = kClusterSize > 1 ? cluster_ctarank() : 0;
     const uint32_t pair_rank = crank % kCtaGroup;   // position inside the CTA pair
-    const uint32_t split_rank = crank / kCtaGroup;  // K slice owned by this CTA
+    const uint32_t split_rank = kSplitK > 1 ? crank / kCtaGroup : 0;  // K slice owned by this CTA
     const bool mma_leader = pair_rank == 0;
     const uint16_t pair_mask = static_cast<uint16_t>(3u << (crank - pair_rank));
+    const uint32_t mc_rank = kMcast > 1 ? crank / kCtaGroup : 0;  // which pair of the multicast cluster
+    const uint16_t mc_all = static_cast<uint16_t>((1u << kClusterSize) - 1);  // every CTA of the cluster
+    const uint16_t mc_a_mask = static_cast<uint16_t>((1u << pair_rank) | (1u << (kCtaGroup + pair_rank)));
 
     if (threadIdx.x == 0 && args.trace) {  // kernel entry (event 7 of unit 0)
         args.trace[(blockIdx.x * 16) * 16 + 7] = global_timer_ns();
@@ -145,7 +154,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     if (threadIdx.x == 32) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], 1);
+            mbar_init(&empty_bar[s], kMcast);  // a release from every pair that reads the slot
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull_bar[b], 1);
@@ -202,7 +211,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 trace_stamp(args, it, 0);
                 ++it;
                 const int m0 = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
-                const int n0 = tn * S::BN_TILE + u.n_off + static_cast<int>(pair_rank) * b_rows;
+                const int n0 = tn * kBNTile + static_cast<int>(mc_rank) * S::BN_TILE + u.n_off +
+                               static_cast<int>(pair_rank) * b_rows;
                 for (int kb = u.k0; kb < u.k1; ++kb) {
                     mbar_wait(&empty_bar[s], ph ^ 1);
                     uint8_t* sa = ring + s * S::STAGE_BYTES;
@@ -218,15 +228,24 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                             else tma_load_2d_pair(dst, map, &full_bar[s], c0, c1);
                         }
                     };
+                    if constexpr (kMcast > 1) {
+                        // my 64-row half of the A block, to me and my rank-twin in the other pair
+                        const int h = static_cast<int>(mc_rank);
+                        if (args.a_mn_major)
+                            tma_load_2d_pair_mc(sa + h * 8192, &tmA, &full_bar[s], m0 + h * 64, k0, mc_a_mask);
+                        else  // tmA box: 64 K x 64 rows for multicast plans
+                            tma_load_2d_pair_mc(sa + h * 8192, &tmA, &full_bar[s], k0, m0 + h * 64, mc_a_mask);
+                    } else {
 #pragma unroll
-                    for (int sl = 0; sl < kSlabs; ++sl) {  // slab sl: rows m0 + sl * BM_MMA
-                        uint8_t* sas = sa + sl * S::SLAB_BYTES;
-                        const int m0s = m0 + sl * S::BM_MMA;
-                        if (args.a_mn_major) {
-                            load(sas, &tmA, m0s, k0, pol_a);
-                            load(sas + 8192, &tmA, m0s + 64, k0, pol_a);
-                        } else {
-                            load(sas, &tmA, k0, m0s, pol_a);
+                        for (int sl = 0; sl < kSlabs; ++sl) {  // slab sl: rows m0 + sl * BM_MMA
+                            uint8_t* sas = sa + sl * S::SLAB_BYTES;
+                            const int m0s = m0 + sl * S::BM_MMA;
+                            if (args.a_mn_major) {
+                                load(sas, &tmA, m0s, k0, pol_a);
+                                load(sas + 8192, &tmA, m0s + 64, k0, pol_a);
+                            } else {
+                                load(sas, &tmA, k0, m0s, pol_a);
+                            }
                         }
                     }
 #pragma unroll
@@ -297,7 +316,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                         }
                     }
                     if constexpr (kCtaGroup == 1) umma_commit(&empty_bar[s]);
-                    else umma_commit_pair(&empty_bar[s], pair_mask);
+                    else umma_commit_pair(&empty_bar[s], kMcast > 1 ? mc_all : pair_mask);
                     if (++s == nst) { s = 0; ph ^= 1; }
                 }
                 if constexpr (kCtaGroup == 1) umma_commit(&tfull_bar[buf]);
@@ -367,7 +386,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             const int nch_all = kSlabs * kNHalves * nchu;
             auto chunk_row = [&](int c) { return kSlabs > 1 ? (c / nchu) * S::BM_MMA : 0; };
             auto chunk_col = [&](int c) {
-                return tn * S::BN_TILE + u.n_off + (kNHalves > 1 ? (c / nchu) * BN : 0) + (c % nchu) * 32;
+                return tn * kBNTile + static_cast<int>(mc_rank) * S::BN_TILE + u.n_off +
+                       (kNHalves > 1 ? (c / nchu) * BN : 0) + (c % nchu) * 32;
             };
             if constexpr (kSplitK == 1) {
                 auto release_tmem = [&] {
@@ -427,8 +447,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                         store_row32_any(args, m + chunk_row(c), chunk_col(c), v);
                     }
                     release_tmem();
-                } else if (kWide) {
-                    // slab / N-half tiles run whole-K units only (the planner never splits them)
+                } else if (kWide || kMcast > 1) {
+                    // slab / N-half / multicast tiles run whole-K units only (never split)
                 } else if (args.sk_pull) {
                     // 2-slice pull fixup. Slice 1 (K-blocks [0, w)) publishes its whole
                     // partial; slice 0 ([w, kb)) streams it back chunk by chunk into
@@ -722,12 +742,12 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     }
 }
 
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves, int kMcast = 1>
 __global__ void __launch_bounds__(256, 1)
     fi_sm100_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
                   const __grid_constant__ GemmArgs args) {
-    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>(tmA, tmB, tmB2, tmC, args);
+    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kMcast>(tmA, tmB, tmB2, tmC, args);
 }
 
 }  // namespace fireiron::sm100

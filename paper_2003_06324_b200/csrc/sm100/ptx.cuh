@@ -160,6 +160,18 @@ __device__ __forceinline__ void tma_load_2d_pair_hint(void* smem_dst, const void
         : "memory");
 }
 
+// 2-CTA load multicast to the CTAs in `mask` (same smem offset in each); every
+// destination pair's leader barrier at the same offset is credited.
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* smem_dst, const void* tmap, uint64_t* bar, int32_t c0,
+                                                    int32_t c1, uint16_t mask) {
+    uint32_t bar_addr = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_addr), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
+
 // 2D tiled bulk-tensor store shared -> global (bulk-group completion).
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(

@@ -25,6 +25,7 @@ struct TcGemmConfig {
     int stages = 0;      // pipeline depth (0 = deepest that fits in shared memory)
     int slabs = 1;       // 2: A slabs per CTA (pair tile 512 x 256, cta_group 2, BN 256)
     int n_halves = 1;    // 2: N halves sharing A (pair tile 256 x 512, cta_group 2, BN 256)
+    int mcast = 1;       // 2: two CTA pairs (neighbours along N) share A stages by TMA multicast
 };
 
 struct TcWorkspace;

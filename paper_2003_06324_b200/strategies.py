@@ -32,10 +32,12 @@ from __future__ import annotations
 def tc_strategy(m: int, n: int, k: int, *, ab: str = "f16", c: str = "f32", pair: bool = True,
                 tile_n: int = 256, split_k: int = 1, stages: int = 0,
                 layouts: tuple = ("colmajor", "colmajor", "colmajor"), swizzle: str = "",
-                tile_m: int = 0) -> str:
+                tile_m: int = 0, multicast: bool = False) -> str:
     """tile_m = 512 (with pair=True, tile_n=256): two A slabs per CTA, the pair
     computes 512 x 256 with two M=256 MMAs per K step sharing B. tile_n = 512
-    (pair, tile_m 256): two N=256 MMAs per K step sharing A via the collector."""
+    (pair, tile_m 256): two N=256 MMAs per K step sharing A via the collector.
+    multicast (pair): two neighbouring pair tiles along N form a 4-CTA cluster
+    and share every A stage through one TMA multicast per half."""
     bm = tile_m or (256 if pair else 128)
     head = f"spec MatMul({m},{n},{k})(GL,GL,GL)(Kernel) elems {ab} {ab} {c}"
     if tuple(layouts) != ("colmajor", "colmajor", "colmajor"):
@@ -45,6 +47,8 @@ def tc_strategy(m: int, n: int, k: int, *, ab: str = "f16", c: str = "f32", pair
         blk += f" .swizzle {swizzle}"
     if pair:
         blk += " .pair"
+    if multicast:
+        blk += " .multicast"
     lines = [head, "", blk]
     if split_k > 1:
         lines.append(f"split {k // split_k} .splitk")
@@ -216,6 +220,8 @@ def sweep_strategies(m: int, n: int, k: int, ab: str = "f16"):
                 continue  # pair 256x64: for narrow problems only
             name = f"tc_{'pair' if pair else 'cta'}_{bm}x{tn}"
             out[name] = tc_strategy(m, n, k, ab=ab, pair=pair, tile_n=tn)
+            if pair and n % (2 * tn) == 0:
+                out[name + "_mcast"] = tc_strategy(m, n, k, ab=ab, pair=True, tile_n=tn, multicast=True)
             tiles = (m // bm) * (n // tn)
             for s in (2, 4):
                 if tiles * s * (2 if pair else 1) <= 148 and k % (64 * s) == 0 and tn // s >= 32 \

@@ -5,7 +5,7 @@
 
 namespace fi_generated {
 using namespace fireiron::sm100;
-constexpr int kCtaGroup = 2, kMmaN = 256, kSplitK = 1, kSlabs = 2, kNHalves = 1;
+constexpr int kCtaGroup = 2, kMmaN = 256, kSplitK = 1, kSlabs = 2, kNHalves = 1, kMcast = 1;
 using Shape = GemmShape<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves>;
 // grid: one persistent CTA per SM (clusters of kCtaGroup*kSplitK), dynamic smem Shape::SMEM_BYTES
 inline GemmArgs matmul_8192x8192x8192_args(void* C) {
@@ -25,6 +25,6 @@ inline GemmArgs matmul_8192x8192x8192_args(void* C) {
 __global__ void __launch_bounds__(256, 1) matmul_8192x8192x8192(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
     const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
     const __grid_constant__ GemmArgs args) {
-  fi_sm100_gemm_body<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves>(tmA, tmB, tmB2, tmC, args);
+  fi_sm100_gemm_body<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves, kMcast>(tmA, tmB, tmB2, tmC, args);
 }
 }  // namespace fi_generated

@@ -90,6 +90,7 @@ MUTANTS = [
     ("unpacked_peer_staging", (768, 1024, 9600), {}, "capacity_errors"),  # 6 slices: staging past the ring
     ("skip_empty_wait", (1024, 1024, 4096), {}, "deadlocks"),             # parity runs ahead of the consumer
     ("tx_undercount", (1024, 1024, 1024), dict(tile_n=512), "deadlocks"),  # N-half tile: B half 2 not expected
+    ("mcast_single_release", (2048, 2048, 2048), dict(multicast=True), "races"),  # twin pair still reading
 ]
 
 
@@ -113,3 +114,14 @@ def test_non_tensor_core_tree_is_rejected(fi):
 def test_pair_256x64_schedules_are_race_free(fi, tc, shape, mode):
     r = fi.check_async(tc(*shape, tile_n=64), streamk=mode)
     assert r.ok, r.text
+
+
+@pytest.mark.parametrize("tn", [64, 128, 256])
+@pytest.mark.parametrize("shape", [(4096, 256, 4096), (2048, 2048, 2048), (1024, 1024, 1024), (4096, 4096, 1024)])
+@pytest.mark.parametrize("layouts", [("colmajor", "colmajor", "colmajor"), ("rowmajor", "colmajor", "colmajor")],
+                         ids=["ccc", "rcc"])
+def test_multicast_pairs_are_race_free(fi, tc, tn, shape, layouts):
+    if shape[1] % (2 * tn):
+        pytest.skip("N must hold two tiles")
+    r = fi.check_async(tc(*shape, tile_n=tn, multicast=True, layouts=layouts))
+    assert r.ok and r.cluster_size == 4 and r.mode == 0, r.text

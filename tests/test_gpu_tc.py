@@ -225,3 +225,30 @@ def test_pair_256x64_tile_integer_exact(fi, oracle, layouts, m, n, k):
     b = oracle.fill(k, n, 42, True)
     want = oracle.gemm_f64(oracle.round_elem(a, "f16"), oracle.round_elem(b, "f16"))
     assert np.array_equal(plan.run_host(a, b), want)
+
+
+@pytest.mark.parametrize("tn", [64, 128, 256])
+@pytest.mark.parametrize("layouts", LAYOUTS, ids=lambda l: "".join(x[0] for x in l))
+def test_multicast_pair_tiles_integer_exact(fi, oracle, tn, layouts):
+    """.multicast: two pair tiles (neighbours along N) form a 4-CTA cluster and
+    share each A stage -- each CTA loads one 64-row half and multicasts it."""
+    if tn == 64 and layouts[1] == "rowmajor":
+        pytest.skip("N = 64 pair tiles need K-major B")
+    m, n, k = 512, 4 * tn, 320
+    s = fi.strategies.tc_strategy(m, n, k, layouts=layouts, tile_n=tn, multicast=True)
+    plan = fi.Plan(s)
+    assert plan.kind == "tcgen05" and plan.info.cluster == 4
+    a = oracle.fill(m, k, 51, True)
+    b = oracle.fill(k, n, 52, True)
+    want = oracle.gemm_f64(oracle.round_elem(a, "f16"), oracle.round_elem(b, "f16"))
+    assert np.array_equal(plan.run_host(a, b), want)
+
+
+def test_multicast_multi_wave_uniform(fi, oracle, monkeypatch):
+    monkeypatch.setenv("FI_HOST_PIPELINE", "0")
+    m = n = 4096
+    k = 1024
+    s = fi.strategies.tc_strategy(m, n, k, multicast=True)
+    c, ar, br = run(fi, oracle, s, m, n, k, False, seed=61)
+    plain = fi.Plan(fi.strategies.tc_strategy(m, n, k))
+    assert np.max(np.abs(plain.run_host(oracle.fill(m, k, 61, False), oracle.fill(k, n, 62, False)) - c)) <= 1e-4
