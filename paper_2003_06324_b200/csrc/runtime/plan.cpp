@@ -293,7 +293,7 @@ int pipeline_chunks(const Plan::Impl& I) {
     if (I.info.kind != 1 || !I.prog.root.is_matmul() || I.tp.tile_order) return 0;
     if (I.tc.b_mn_major || I.tc.c_row_major) return 0;  // panels must be contiguous column ranges
     if (const char* e = std::getenv("FI_HOST_PIPELINE"); e && e[0] == '0') return 0;
-    const long tiles_n = I.tp.N / I.tc.bn;
+    const long tiles_n = I.tp.N / (I.tc.bn * I.tc.n_halves * I.tc.mcast);  // whole scheduled tiles per panel
     const double b_bytes = 4.0 * I.tp.K * I.tp.N;
     int best = 0;
     for (int p = 2; p <= 8; ++p)  // panels of >= 4 MiB each, whole block tiles

@@ -1,0 +1,73 @@
+"""Randomised GPU parity over the tcgen05 strategy space: tile variant (1-CTA,
+pair, 512x256 slabs, 256x512 N halves, multicast pairs), tile N, split-K,
+pipeline depth, operand layouts, C element type and problem shape, drawn with
+a fixed seed. Every case must be integer-exact against the fp64 oracle at
+sampled points (C in f16/bf16: exact after rounding the oracle) and must pass
+the CPU protocol checker first."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+LAYOUTS = [("colmajor", "colmajor", "colmajor"), ("rowmajor", "colmajor", "colmajor"),
+           ("colmajor", "rowmajor", "rowmajor"), ("rowmajor", "rowmajor", "colmajor")]
+
+
+def draw(rng):
+    kind = rng.choice(["cta", "pair", "slab", "nhalf", "mcast"], p=[0.25, 0.35, 0.1, 0.1, 0.2])
+    kw = {}
+    if kind == "cta":
+        kw.update(pair=False, tile_n=int(rng.choice([64, 128, 256])))
+        bm, bn = 128, kw["tile_n"]
+    elif kind == "pair":
+        kw.update(pair=True, tile_n=int(rng.choice([64, 128, 256])))
+        bm, bn = 256, kw["tile_n"]
+    elif kind == "slab":
+        kw.update(pair=True, tile_n=256, tile_m=512)
+        bm, bn = 512, 256
+    elif kind == "nhalf":
+        kw.update(pair=True, tile_n=512)
+        bm, bn = 256, 512
+    else:
+        kw.update(pair=True, tile_n=int(rng.choice([64, 128, 256])), multicast=True)
+        bm, bn = 256, 2 * kw["tile_n"]
+    lay = LAYOUTS[int(rng.integers(0, 4))]
+    if kw["tile_n"] == 64 and kw["pair"] and lay[1] == "rowmajor":
+        lay = LAYOUTS[int(rng.integers(0, 2))]  # N = 64 pair tiles need K-major B
+    kw["layouts"] = lay
+    m = bm * int(rng.integers(1, max(2, 2048 // bm) + 1))
+    n = bn * int(rng.integers(1, max(2, 2048 // bn) + 1))
+    k = 64 * int(rng.integers(1, 33))
+    if kind in ("cta", "pair") and rng.random() < 0.3:
+        s = int(rng.choice([2, 4]))
+        if k % (64 * s) == 0 and (kw["tile_n"] // s) >= 32 and not (kind == "pair" and kw["tile_n"] == 64):
+            kw["split_k"] = s
+    if rng.random() < 0.3:
+        kw["stages"] = int(rng.integers(2, 5))
+    kw["c"] = str(rng.choice(["f32", "f32", "f16", "bf16"]))
+    return m, n, k, kw
+
+
+CASES = []
+_rng = np.random.default_rng(20261017)
+while len(CASES) < 80:
+    CASES.append(draw(_rng))
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_random_tcgen05_strategy(fi, oracle, case):
+    m, n, k, kw = CASES[case]
+    script = fi.strategies.tc_strategy(m, n, k, **kw)
+    chk = fi.check_async(script)
+    assert chk.ok, (kw, chk.text)
+    plan = fi.Plan(script)
+    assert plan.kind == "tcgen05"
+    a = oracle.fill(m, k, 100 + case, True)
+    b = oracle.fill(k, n, 200 + case, True)
+    c = plan.run_host(a, b)
+    rng = np.random.default_rng(case)
+    rows, cols = rng.integers(0, m, 2048), rng.integers(0, n, 2048)
+    want = oracle.sample_f64(oracle.round_elem(a, "f16"), oracle.round_elem(b, "f16"), rows, cols).astype(np.float32)
+    if kw["c"] != "f32":
+        want = oracle.round_elem(want, kw["c"])
+    assert np.array_equal(c[rows, cols], want), (m, n, k, kw)
