@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libfireiron_b200.so")
+LIB_PATH = os.environ.get("FI_LIB_PATH") or os.path.join(_HERE, "_lib", "libfireiron_b200.so")  # override: A/B builds
 
 FI_OK = 0
 FI_F32, FI_F16, FI_BF16 = 0, 1, 2
