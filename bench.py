@@ -293,7 +293,25 @@ def ours_multi(args, fi, torch, rank, world):
     # NCCL per-owner broadcasts (FI_DIST_TRANSPORT=nccl), or direct TMA reads of
     # the owners' buffers from inside the chunk GEMMs (FI_DIST_TRANSPORT=direct)
     transport = os.environ.get("FI_DIST_TRANSPORT", "peer")
-    pg = PeerGather(shard, Bf, dist) if transport in ("peer", "direct") else None
+    pg = None
+    if transport in ("peer", "direct"):
+        # every rank must map every peer's buffer; if any rank cannot (no IPC /
+        # P2P between these GPUs), all ranks fall back to NCCL broadcasts
+        err = None
+        try:
+            pg = PeerGather(shard, Bf, dist)
+        except Exception as e:  # noqa: BLE001 - reported below, decided collectively
+            err = e
+        ok = torch.tensor([0 if err else 1], device=dev, dtype=torch.int32)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 0:
+            if pg is not None:
+                pg.close()
+                pg = None
+            if rank == 0:
+                print(f"bench: CUDA IPC transport unavailable ({err or 'on a peer rank'}); using NCCL broadcasts",
+                      file=sys.stderr)
+            transport = "nccl"
 
     def gemm_ptr(j, a, bptr, c):
         plan.launch(a.data_ptr(), bptr, c.data_ptr(), stream.cuda_stream)

@@ -248,7 +248,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
                          args.streamk, tiles, kb);
             // cta unit t0 t1 t2 t3 clk0 clk1 t4 t5 t6 clk2 clk6 t7 (globaltimer ns, clock64)
             for (size_t i = 0; i < trace_n; i += 16)
-                if (h[i] || h[i + 2])
+                if (h[i] || h[i + 2] || h[i + 7])
                     std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 256,
                                  (i / 16) % 16, h[i], h[i + 1], h[i + 2], h[i + 3], h[i + 8], h[i + 9], h[i + 4], h[i + 5],
                                  h[i + 6], h[i + 10], h[i + 14], h[i + 7]);

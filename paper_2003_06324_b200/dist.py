@@ -104,10 +104,16 @@ class PeerGather:
         self.shard, self.N, self.C = shard, N, C
         h = (C.c_char * 64)()
         off = C.c_int64()
-        N.check(N.lib.fi_ipc_export(C.c_void_p(b_full.data_ptr()), h, C.byref(off)))
+        mine = None
+        if N.lib.fi_ipc_export(C.c_void_p(b_full.data_ptr()), h, C.byref(off)) == 0:
+            mine = (bytes(h), off.value)
+        # the exchange is reached by every rank even when an export failed, so a
+        # failure raises on every rank instead of leaving peers in the collective
         objs = [None] * shard.world
-        dist.all_gather_object(objs, (bytes(h), off.value))
+        dist.all_gather_object(objs, mine)
         self.peer = {}
+        if any(o is None for o in objs):
+            raise RuntimeError("fi_ipc_export failed on rank(s) %s" % [j for j, o in enumerate(objs) if o is None])
         for j, (hb, o) in enumerate(objs):
             if j == shard.rank:
                 continue

@@ -72,3 +72,34 @@ def test_shard_geometry():
     assert sh.order()[0] == 3
     with pytest.raises(ValueError):
         make_shard(1000, 1000, 64, 8, 0)
+
+
+def _ipc_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2003_06324_b200.dist import PeerGather
+    sh = make_shard(16, 24, 12, world, rank, tile_m=4, tile_n=4)
+    try:
+        PeerGather(sh, torch.zeros(12 * 24), dist)  # host memory: the export fails on every rank
+        q.put((rank, "no error"))
+    except RuntimeError as e:
+        q.put((rank, str(e)))
+    dist.destroy_process_group()
+
+
+def test_peer_gather_failure_is_collective():
+    """A rank whose CUDA IPC export fails must not strand its peers inside the
+    handle exchange: every rank raises, so bench.py can agree on the NCCL
+    fallback."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(res) == [0, 1]
+    assert all("fi_ipc_export failed" in v for v in res.values()), res
