@@ -84,4 +84,79 @@ cudaError_t widen_to_f32(const void* src, float* dst, int64_t n, int elem, cudaS
     return cudaGetLastError();
 }
 
+// Pitched regions (width contiguous elements x height lines, `pitch` elements
+// apart; source and destination share the pitch): the blocked host pipeline
+// converts each operand panel and widens each C block where it lands.
+template <typename T, bool kVec>
+__global__ void convert_2d_kernel(const float* __restrict__ src, T* __restrict__ dst, int64_t width, int64_t height,
+                                  int64_t pitch) {
+    constexpr int V = kVec ? 4 : 1;
+    const int64_t per_line = width / V;
+    const int64_t n = per_line * height;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t y = i / per_line, x = (i - y * per_line) * V;
+        const int64_t o = y * pitch + x;
+        if constexpr (kVec) {
+            const float4 v = *reinterpret_cast<const float4*>(src + o);
+            dst[o] = cvt<T>(v.x);
+            dst[o + 1] = cvt<T>(v.y);
+            dst[o + 2] = cvt<T>(v.z);
+            dst[o + 3] = cvt<T>(v.w);
+        } else {
+            dst[o] = cvt<T>(src[o]);
+        }
+    }
+}
+
+template <typename T>
+__global__ void widen_2d_kernel(const T* __restrict__ src, float* __restrict__ dst, int64_t width, int64_t height,
+                                int64_t pitch) {
+    const int64_t n = width * height;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t y = i / width, o = y * pitch + (i - y * width);
+        dst[o] = widen<T>(src[o]);
+    }
+}
+
+cudaError_t convert_f32_2d(const float* src, void* dst, int64_t width, int64_t height, int64_t pitch, int elem,
+                           cudaStream_t s) {
+    if (width <= 0 || height <= 0) return cudaSuccess;
+    if (elem == 0)
+        return cudaMemcpy2DAsync(dst, pitch * 4, src, pitch * 4, width * 4, height, cudaMemcpyDeviceToDevice, s);
+    const bool vec = width % 4 == 0 && pitch % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    const int g = grid_for(width * height);
+    switch (elem * 2 + (vec ? 1 : 0)) {
+        case 2: convert_2d_kernel<__half, false><<<g, 256, 0, s>>>(src, static_cast<__half*>(dst), width, height, pitch); break;
+        case 3: convert_2d_kernel<__half, true><<<g, 256, 0, s>>>(src, static_cast<__half*>(dst), width, height, pitch); break;
+        case 4:
+            convert_2d_kernel<__nv_bfloat16, false>
+                <<<g, 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), width, height, pitch);
+            break;
+        case 5:
+            convert_2d_kernel<__nv_bfloat16, true>
+                <<<g, 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), width, height, pitch);
+            break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t widen_to_f32_2d(const void* src, float* dst, int64_t width, int64_t height, int64_t pitch, int elem,
+                            cudaStream_t s) {
+    if (width <= 0 || height <= 0) return cudaSuccess;
+    const int g = grid_for(width * height * 4);
+    switch (elem) {
+        case 0: return cudaMemcpy2DAsync(dst, pitch * 4, src, pitch * 4, width * 4, height, cudaMemcpyDeviceToDevice, s);
+        case 1: widen_2d_kernel<__half><<<g, 256, 0, s>>>(static_cast<const __half*>(src), dst, width, height, pitch); break;
+        case 2:
+            widen_2d_kernel<__nv_bfloat16>
+                <<<g, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(src), dst, width, height, pitch);
+            break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace fireiron::rt

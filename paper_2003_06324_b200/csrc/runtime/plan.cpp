@@ -26,6 +26,10 @@ long generic_shared_bytes(const Program& prog);
 namespace rt {
 cudaError_t convert_f32(const float* src, void* dst, int64_t n, int elem, cudaStream_t s);
 cudaError_t widen_to_f32(const void* src, float* dst, int64_t n, int elem, cudaStream_t s);
+cudaError_t convert_f32_2d(const float* src, void* dst, int64_t width, int64_t height, int64_t pitch, int elem,
+                           cudaStream_t s);
+cudaError_t widen_to_f32_2d(const void* src, float* dst, int64_t width, int64_t height, int64_t pitch, int elem,
+                            cudaStream_t s);
 int device_sm_count();
 }  // namespace rt
 
@@ -292,13 +296,177 @@ namespace {
 int pipeline_chunks(const Plan::Impl& I) {
     if (I.info.kind != 1 || !I.prog.root.is_matmul() || I.tp.tile_order) return 0;
     if (I.tc.b_mn_major || I.tc.c_row_major) return 0;  // panels must be contiguous column ranges
-    if (const char* e = std::getenv("FI_HOST_PIPELINE"); e && e[0] == '0') return 0;
+    if (const char* e = std::getenv("FI_HOST_PIPELINE"); e && (e[0] == '0' || e[0] == 'b')) return 0;
     const long tiles_n = I.tp.N / (I.tc.bn * I.tc.n_halves * I.tc.mcast);  // whole scheduled tiles per panel
     const double b_bytes = 4.0 * I.tp.K * I.tp.N;
-    int best = 0;
-    for (int p = 2; p <= 8; ++p)  // panels of >= 4 MiB each, whole block tiles
+    int best = 0, cap = 8;
+    if (const char* v = std::getenv("FI_HOST_PANELS")) cap = std::atoi(v);
+    for (int p = 2; p <= cap; ++p)  // panels of >= 4 MiB each, whole block tiles
         if (tiles_n % p == 0 && b_bytes / p >= 4.0 * (1 << 20)) best = p;
     return best;
+}
+
+// ---------------------------------------------------------------- blocked run_host
+// The column-panel pipeline above still uploads all of A before the first GEMM.
+// The blocked pipeline cuts A into P row panels and B into Q column panels and
+// uploads them alternately (balanced by bytes); as each panel lands, ONE GEMM
+// computes the C blocks it completes -- row panel i against the B panels already
+// up, or the A panels already up against column panel j -- and that C region
+// goes down while later panels come up. The first GEMM waits for one panel of
+// each operand, so PCIe runs both directions for most of the call. Panels and
+// C regions are pitched 2D copies, so any root layout qualifies.
+struct Region {
+    long off, width, height, pitch;  // elements: `height` lines of `width`, `pitch` apart
+};
+
+bool blocked_split(const Plan::Impl& I, int& P, int& Q) {
+    if (I.info.kind != 1 || !I.prog.root.is_matmul() || I.tp.tile_order) return false;
+    const char* e = std::getenv("FI_HOST_PIPELINE");
+    if (e && (e[0] == '0' || e[0] == 'p')) return false;  // off, or the column-panel pipeline
+    const long tm = 128L * I.tc.cta_group * I.tc.slabs;
+    const long tn = static_cast<long>(I.tc.bn) * I.tc.n_halves * I.tc.mcast;
+    double piece = 16.0 * (1 << 20);  // target panel size: 16 MiB of fp32 (measured: profiles/round1/e2e_host_pipeline.txt)
+    if (const char* v = std::getenv("FI_HOST_PANEL_MB")) piece = std::atof(v) * (1 << 20);
+    // a panel cut across the contiguous dimension is a pitched copy whose lines
+    // must stay >= 4 KiB: shorter lines cost PCIe duplex bandwidth (2 KiB lines:
+    // 62 GB/s both ways vs 99 linear, profiles/round1/e2e_host_pipeline.txt)
+    const bool a_strided = I.tc.a_mn_major || I.tc.c_row_major == 0;  // A or C lines of M/P elements
+    const bool b_strided = I.tc.b_mn_major || I.tc.c_row_major != 0;  // B or C lines of N/Q elements
+    long min_line = 1024;
+    if (const char* v = std::getenv("FI_HOST_MIN_LINE")) min_line = std::atol(v);
+    auto pick = [&](long dim, long tile, double bytes, bool strided) {
+        int best = 1;
+        for (int p = 2; p <= 64; ++p)
+            if (dim % (p * tile) == 0 && bytes / p >= piece && (!strided || dim / p >= min_line)) best = p;
+        return best;
+    };
+    // measured crossover: 4096^3 (128 MiB up) blocked 3.08 ms vs column panels
+    // 3.5-3.7; 1024^2 x 32768 (256 MiB) equal; 16384^3 (2 GiB) blocked 47.4 ms vs
+    // 45.7 (there the pitched A copies cost more than the early C download gains)
+    double up_limit = 512.0 * (1 << 20);
+    if (const char* v = std::getenv("FI_HOST_BLOCKED_MAX_MB")) up_limit = std::atof(v) * (1 << 20);
+    if (4.0 * I.tp.K * (static_cast<double>(I.tp.M) + I.tp.N) > up_limit) return false;
+    P = pick(I.tp.M, tm, 4.0 * I.tp.M * I.tp.K, a_strided);
+    Q = pick(I.tp.N, tn, 4.0 * I.tp.K * I.tp.N, b_strided);
+    return P * Q >= 4;
+}
+
+double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, float* C, cudaStream_t s, int P,
+                        int Q, char* base, const size_t* f32_in, const size_t* typed_in, size_t typed_c,
+                        size_t f32_c) {
+    if (!I.up_stream) {
+        ck(cudaStreamCreateWithFlags(&I.up_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&I.down_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+    const int np = P + Q;
+    // events: [start][upload per panel][gemm begin, end per panel][C ready per panel][down done]
+    const size_t need = 1 + np + 2 * np + np + 1;
+    while (I.pev.size() < need) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        I.pev.push_back(e);
+    }
+    cudaEvent_t* ev = I.pev.data();
+    cudaEvent_t ev_start = ev[0], *ev_up = ev + 1, *ev_g = ev_up + np, *ev_c = ev_g + 2 * np, ev_down = ev_c[np];
+    const BufferDecl& ra = I.root(0);
+    const BufferDecl& rb = I.root(1);
+    const BufferDecl& rc = I.root(2);
+    const int ea = elem_code(ra.elem), eb = elem_code(rb.elem), ec = elem_code(rc.elem);
+    const size_t wa = byte_width(ra.elem), wb = byte_width(rb.elem), wc = byte_width(rc.elem);
+    const long M = I.tp.M, N = I.tp.N, K = I.tp.K, lda = I.tp.lda, ldb = I.tp.ldb, ldc = I.tp.ldc;
+    const bool a_row = !I.tc.a_mn_major, b_row = I.tc.b_mn_major != 0, c_row = I.tc.c_row_major != 0;
+    const long mc = M / P, nc = N / Q;
+    auto a_region = [&](long r0, long r1) { return a_row ? Region{r0 * lda, K, r1 - r0, lda} : Region{r0, r1 - r0, K, lda}; };
+    auto b_region = [&](long c0, long c1) { return b_row ? Region{c0, c1 - c0, K, ldb} : Region{c0 * ldb, K, c1 - c0, ldb}; };
+    auto c_region = [&](long r0, long r1, long c0, long c1) {
+        return c_row ? Region{r0 * ldc + c0, c1 - c0, r1 - r0, ldc} : Region{r0 + c0 * ldc, r1 - r0, c1 - c0, ldc};
+    };
+    auto copy2d = [&](void* dst, const void* src, const Region& r, cudaMemcpyKind kind, cudaStream_t st) {
+        if (r.width == r.pitch)  // contiguous lines: one linear copy
+            ck(cudaMemcpyAsync(dst, src, static_cast<size_t>(r.width * r.height) * 4, kind, st), "cudaMemcpyAsync");
+        else
+            ck(cudaMemcpy2DAsync(dst, r.pitch * 4, src, r.pitch * 4, r.width * 4, r.height, kind, st),
+               "cudaMemcpy2DAsync");
+    };
+    ck(cudaEventRecord(ev_start, s), "cudaEventRecord");  // scratch reuse: after earlier work on s
+    ck(cudaStreamWaitEvent(I.up_stream, ev_start, 0), "cudaStreamWaitEvent");
+    ck(cudaStreamWaitEvent(I.down_stream, ev_start, 0), "cudaStreamWaitEvent");
+    // one panel: H2D into the fp32 staging (or straight into an fp32 root), then
+    // snapped to the root's element grid on s (sim.hpp:507-510)
+    auto upload = [&](int which, const float* host, const Region& r, int elem, size_t w, cudaEvent_t done) {
+        char* typed = base + typed_in[which];
+        float* stage = elem == 0 ? reinterpret_cast<float*>(typed) : reinterpret_cast<float*>(base + f32_in[which]);
+        copy2d(stage + r.off, host + r.off, r, cudaMemcpyHostToDevice, I.up_stream);
+        ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(s, done, 0), "cudaStreamWaitEvent");
+        if (elem != 0)
+            ck(rt::convert_f32_2d(stage + r.off, typed + static_cast<size_t>(r.off) * w, r.width, r.height, r.pitch, elem, s),
+               "input conversion");
+    };
+    int ng = 0;
+    auto gemm = [&](long r0, long r1, long c0, long c1) {
+        sm100::TcGemmProblem p = I.tp;
+        p.workspace = &I.ws;
+        p.A = base + typed_in[0] + static_cast<size_t>(a_region(r0, r1).off) * wa;
+        p.B = base + typed_in[1] + static_cast<size_t>(b_region(c0, c1).off) * wb;
+        const Region cr = c_region(r0, r1, c0, c1);
+        p.C = base + typed_c + static_cast<size_t>(cr.off) * wc;
+        p.M = static_cast<int>(r1 - r0);
+        p.N = static_cast<int>(c1 - c0);
+        ck(cudaEventRecord(ev_g[2 * ng], s), "cudaEventRecord");
+        const int r = sm100::tc_gemm_launch(I.tc, p, s);
+        if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+        ck(cudaEventRecord(ev_g[2 * ng + 1], s), "cudaEventRecord");
+        const float* result = reinterpret_cast<const float*>(base + typed_c);
+        if (ec != 0) {
+            ck(rt::widen_to_f32_2d(base + typed_c + static_cast<size_t>(cr.off) * wc,
+                                   reinterpret_cast<float*>(base + f32_c) + cr.off, cr.width, cr.height, cr.pitch, ec, s),
+               "output conversion");
+            result = reinterpret_cast<const float*>(base + f32_c);
+        }
+        ck(cudaEventRecord(ev_c[ng], s), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(I.down_stream, ev_c[ng], 0), "cudaStreamWaitEvent");
+        copy2d(C + cr.off, result + cr.off, cr, cudaMemcpyDeviceToHost, I.down_stream);
+        ++ng;
+    };
+    const double a_piece = 4.0 * mc * K, b_piece = 4.0 * K * nc;
+    int ia = 0, ib = 0;
+    std::vector<char> order;
+    while (ia < P || ib < Q) {
+        const bool take_a = ib == Q || (ia < P && ia * a_piece <= ib * b_piece);
+        if (take_a) {
+            upload(0, A, a_region(ia * mc, (ia + 1) * mc), ea, wa, ev_up[ia + ib]);
+            ++ia;
+            if (ib > 0) gemm((ia - 1) * mc, ia * mc, 0, ib * nc);
+        } else {
+            upload(1, B, b_region(ib * nc, (ib + 1) * nc), eb, wb, ev_up[ia + ib]);
+            ++ib;
+            if (ia > 0) gemm(0, ia * mc, (ib - 1) * nc, ib * nc);
+        }
+        order.push_back(take_a ? 'A' : 'B');
+    }
+    ck(cudaEventRecord(ev_down, I.down_stream), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(s, ev_down, 0), "cudaStreamWaitEvent");
+    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    float ms_total = 0.f;
+    for (int g = 0; g < ng; ++g) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev_g[2 * g], ev_g[2 * g + 1]);
+        ms_total += ms;
+    }
+    if (std::getenv("FI_HOST_PIPELINE_TRACE")) {  // event timeline relative to the start (ms)
+        auto at = [&](cudaEvent_t e) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev_start, e);
+            return ms;
+        };
+        std::fprintf(stderr, "blocked %dx%d panels: up", P, Q);
+        for (int i = 0; i < np; ++i) std::fprintf(stderr, " %c%.3f", order[static_cast<size_t>(i)], at(ev_up[i]));
+        std::fprintf(stderr, " | gemm");
+        for (int g = 0; g < ng; ++g) std::fprintf(stderr, " %.3f-%.3f", at(ev_g[2 * g]), at(ev_g[2 * g + 1]));
+        std::fprintf(stderr, " | C down done %.3f\n", at(ev_down));
+    }
+    return ms_total;
 }
 
 double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, float* C, cudaStream_t s,
@@ -608,6 +776,8 @@ double Plan::run_host_raw(const float* A, const float* B, float* C, void* stream
         ck(cudaEventCreate(&I.ev0), "cudaEventCreate");
         ck(cudaEventCreate(&I.ev1), "cudaEventCreate");
     }
+    if (int P = 0, Q = 0; blocked_split(I, P, Q))
+        return run_host_blocked(I, A, B, C, s, P, Q, base, f32_in, typed_in, typed_c, f32_c);
     if (const int chunks = pipeline_chunks(I); chunks > 0)
         return run_host_pipelined(I, A, B, C, s, chunks, base, f32_in, typed_in, typed_c, f32_c);
     for (int i = 0; i < nin; ++i) {

@@ -207,16 +207,20 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         const size_t slots = static_cast<size_t>(plan.slots);
         const size_t need_p = slots * kCtaGroup * S::WS_FLOATS;
         const size_t need_f = slots * kCtaGroup;
+        // growth is stream-ordered (cudaFreeAsync / cudaMallocAsync): a launch that
+        // needs a larger workspace must not synchronise the device, e.g. inside
+        // the host pipeline while uploads are still in flight
         if (ws->partial_floats < need_p) {
-            if (ws->partials) cudaFree(ws->partials);
+            const size_t grow = need_p + need_p / 4;
+            if (ws->partials) cudaFreeAsync(ws->partials, stream);
             ws->partials = nullptr;
-            if (cudaMalloc(&ws->partials, need_p * sizeof(float)) != cudaSuccess) return kTcErrCuda;
-            ws->partial_floats = need_p;
+            if (cudaMallocAsync(&ws->partials, grow * sizeof(float), stream) != cudaSuccess) return kTcErrCuda;
+            ws->partial_floats = grow;
         }
         if (ws->flag_count < need_f) {
-            if (ws->flags) cudaFree(ws->flags);
+            if (ws->flags) cudaFreeAsync(ws->flags, stream);
             ws->flags = nullptr;
-            if (cudaMalloc(&ws->flags, need_f * sizeof(unsigned)) != cudaSuccess) return kTcErrCuda;
+            if (cudaMallocAsync(&ws->flags, need_f * sizeof(unsigned), stream) != cudaSuccess) return kTcErrCuda;
             if (cudaMemsetAsync(ws->flags, 0, need_f * sizeof(unsigned), stream) != cudaSuccess) return kTcErrCuda;
             ws->flag_count = need_f;
             ws->epoch = 0;
