@@ -621,7 +621,7 @@ private:
                     long slot = u.slot;
                     if (remainder && opt_.mutation == kMutRemainderSlotCollision) slot = ncl_ - 1;
                     const long peer0 = static_cast<long>(nown) * kChunkBytes;  // ring offset of the peer region
-                    if (!remainder) {
+                    if (!remainder || (last_unit && a_.ring_drain)) {
                         auto slot_off = [&](int c) {
                             const bool mine = c >= c_lo && c < c_hi;
                             return mine ? static_cast<long>(c - c_lo) * kChunkBytes

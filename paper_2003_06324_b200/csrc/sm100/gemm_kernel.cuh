@@ -551,8 +551,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     // chunks [c_lo, c_hi) and keeps those in smem (a main slice is the
                     // cluster's last unit: its operand ring is idle); every other chunk
                     // is published in its workspace slot. A remainder slice owns no
-                    // columns and publishes all of them (its ring stays in use by the
-                    // next remainder unit). Each owner then sums its range over all
+                    // columns and publishes all of them (through the epi buffers while
+                    // its ring is still in use by a next remainder unit). Each owner then sums its range over all
                     // sources in K order (slices 0..S-1, then the remainder) and
                     // stores it: deterministic, and the S fixups run in parallel.
                     const int nslc = args.sk_slices, s = u.slice;
@@ -572,8 +572,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     float* peer = own + nown * kChunkFloats;       // [nsrc-1][nown][32][128]
                     float* slot_ws = args.workspace + static_cast<long>(u.slot * kCtaGroup + pair_rank) * S::WS_FLOATS;
                     // publish: every chunk that is not mine goes to the workspace slot
-                    // as one 16 KB bulk copy out of shared memory
-                    if (!remainder) {
+                    // as one 16 KB bulk copy out of shared memory. A remainder unit
+                    // that is its cluster's last unit drains through the idle ring too
+                    // (all copies in flight at once instead of two epi buffers)
+                    if (!remainder || (last_unit && args.ring_drain)) {
                         auto slot = [&](int c) {
                             const bool mine = c >= c_lo && c < c_hi;
                             return mine ? own + (c - c_lo) * kChunkFloats
