@@ -7,6 +7,10 @@
 //                                 cluster and receive each A stage by one TMA multicast
 //   split K .stages S          -> S-deep TMA/MMA mbarrier pipeline over the K loop
 //   split K .splitk            -> the split's chunks run in parallel on the CTAs
+//   split K .prefetchLoads / .doubleBufferLoop, load .. .doubleBuffer / .postponed
+//                              -> the paper's pipelining refinements: the
+//                                 deepest / a 2-stage TMA ring; postponed loads are what the
+//                                 warp-specialised producer does. Scheduling only.
 //                                 of a cluster; the following epilog reduces the
 //                                 partial accumulators on chip (paper's splitK,
 //                                 PAPER.md:67-127)
@@ -43,6 +47,10 @@ struct LoadRefinements {
     long pad = 0;
     std::optional<long> align;
     bool reuse_buffer = false;
+    // paper appendix, scheduling only -- results are unchanged:
+    bool double_buffer = false;   // .doubleBuffer: two staging buffers (sm_100a SH loads: a 2-stage TMA ring)
+    bool postponed = false;       // .postponed: the next step's loads complete behind this step's MMA
+                                  // (sm_100a: the TMA producer warp always runs ahead of the MMA warp)
 };
 
 struct SplitRefinements {
@@ -50,6 +58,9 @@ struct SplitRefinements {
     bool sync = false;
     int stages = 0;        // sm_100a: pipeline depth (0 = default)
     bool splitk = false;   // sm_100a: parallel split with on-chip reduction
+    // paper appendix, scheduling only:
+    bool prefetch = false;       // .prefetchLoads: loads of later steps in flight (the deepest ring, stages 0)
+    bool double_buffer = false;  // .doubleBufferLoop: two stages (normalised to stages = 2)
 };
 
 enum class NodeKind { Tile, Split, Load, Epilog, MmaTile, Done };

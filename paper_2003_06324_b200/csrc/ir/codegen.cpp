@@ -447,12 +447,20 @@ TcStrategy match_tc_strategy(const Spec& root, const NodePtr& tree, const MicroK
         return reject("expected the pipelined K split after the epilog");
     if (kl->split_k != 64) return reject("the K block must be 64 (one 128B swizzle span of 16-bit elements)");
     tc.tile_k = 64;
-    tc.stages = kl->split_ref.stages;
+    tc.stages = kl->split_ref.stages;  // .prefetchLoads: 0 = the deepest ring that fits
     bool have_a = false, have_b = false;
     for (int j = 0; j < 2; ++j) {
         const DecompNode* ld = at(i++);
         if (!ld || ld->kind != NodeKind::Load || ld->target.kind != MemKind::SH)
             return reject("expected loads of A and B into SH");
+        // A and B share each ring stage: a double-buffered operand makes the ring 2 deep
+        if (ld->load_ref.double_buffer) {
+            if (tc.stages != 0 && tc.stages != 2)
+                return reject("load .doubleBuffer is a 2-stage TMA ring; it conflicts with .stages " +
+                              std::to_string(tc.stages));
+            if (kl->split_ref.prefetch) return reject("load .doubleBuffer conflicts with .prefetchLoads");
+            tc.stages = 2;
+        }
         if (ld->load_ref.pad || ld->load_ref.storage_layout || ld->load_ref.reuse_buffer || ld->load_ref.align)
             return reject("TMA loads use the 128B-swizzled layout; pad/storagelayout/align/reusebuffer do not apply");
         auto mv = chain_nodes(ld->move_decomp);

@@ -332,6 +332,8 @@ NodePtr parse_step(Cursor& cur, const Line& ln, NodePtr prev) {
             if (kw == ".unroll") ref.unroll = true;
             else if (kw == ".sync") ref.sync = true;
             else if (kw == ".splitk") ref.splitk = true;
+            else if (kw == ".prefetchloads") ref.prefetch = true;
+            else if (kw == ".doublebufferloop") ref.double_buffer = true;
             else if (kw == ".stages") {
                 ref.stages = static_cast<int>(int_token(ln, i + 1, "stage count"));
                 i += 2;
@@ -372,6 +374,12 @@ NodePtr parse_step(Cursor& cur, const Line& ln, NodePtr prev) {
                 ++i;
             } else if (k == ".reusebuffer") {
                 ref.reuse_buffer = true;
+                ++i;
+            } else if (k == ".doublebuffer") {
+                ref.double_buffer = true;
+                ++i;
+            } else if (k == ".postponed") {
+                ref.postponed = true;
                 ++i;
             } else {
                 parse_fail(ln.number, t[i].col, "unknown load refinement '" + t[i].text + "'");
@@ -610,7 +618,9 @@ void print_chain(const NodePtr& node, std::string& out, int indent) {
                 std::string l = pad + "split " + std::to_string(n->split_k);
                 if (n->split_ref.unroll) l += " .unroll";
                 if (n->split_ref.sync) l += " .sync";
-                if (n->split_ref.stages > 0) l += " .stages " + std::to_string(n->split_ref.stages);
+                if (n->split_ref.double_buffer) l += " .doubleBufferLoop";
+                else if (n->split_ref.stages > 0) l += " .stages " + std::to_string(n->split_ref.stages);
+                if (n->split_ref.prefetch) l += " .prefetchLoads";
                 if (n->split_ref.splitk) l += " .splitk";
                 out += l + "\n";
                 break;
@@ -623,6 +633,8 @@ void print_chain(const NodePtr& node, std::string& out, int indent) {
                 if (n->load_ref.align) l += " .align " + std::to_string(*n->load_ref.align);
                 if (n->load_ref.no_sync) l += " .nosync";
                 if (n->load_ref.reuse_buffer) l += " .reusebuffer";
+                if (n->load_ref.double_buffer) l += " .doubleBuffer";
+                if (n->load_ref.postponed) l += " .postponed";
                 out += l + " {\n";
                 print_chain(n->move_decomp, out, indent + 1);
                 out += pad + "}\n";
