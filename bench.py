@@ -270,7 +270,8 @@ def ours_single(args, fi, torch):
 
 def ours_multi(args, fi, torch, rank, world):
     import torch.distributed as dist
-    from paper_2003_06324_b200.dist import PeerGather, make_shard, sharded_step, sharded_step_direct, sharded_step_peer
+    from paper_2003_06324_b200.dist import (PeerGather, make_shard, sharded_step, sharded_step_direct,
+                                            sharded_step_fused, sharded_step_peer)
     wl = workload_of(args, world)
     m, n, k = wl["m"], wl["n"], wl["k"]
     shard = make_shard(m, n, k, world, rank)
@@ -289,12 +290,13 @@ def ours_multi(args, fi, torch, rank, world):
     def gemm(j, a, b, c):
         plan.launch(a.data_ptr(), b.data_ptr(), c.data_ptr(), stream.cuda_stream)
 
-    # B transport: copy-engine pulls from IPC-mapped peer buffers (default),
-    # NCCL per-owner broadcasts (FI_DIST_TRANSPORT=nccl), or direct TMA reads of
-    # the owners' buffers from inside the chunk GEMMs (FI_DIST_TRANSPORT=direct)
-    transport = os.environ.get("FI_DIST_TRANSPORT", "peer")
+    # B transport: copy-engine pulls releasing per-chunk flags to ONE gated
+    # persistent GEMM over the whole band (default, "fused"), copy-engine pulls
+    # with one GEMM per chunk ("peer"), NCCL per-owner broadcasts ("nccl"), or
+    # direct TMA reads of the owners' buffers inside the chunk GEMMs ("direct")
+    transport = os.environ.get("FI_DIST_TRANSPORT", "fused")
     pg = None
-    if transport in ("peer", "direct"):
+    if transport in ("peer", "direct", "fused"):
         # every rank must map every peer's buffer; if any rank cannot (no IPC /
         # P2P between these GPUs), all ranks fall back to NCCL broadcasts
         err = None
@@ -316,8 +318,15 @@ def ours_multi(args, fi, torch, rank, world):
     def gemm_ptr(j, a, bptr, c):
         plan.launch(a.data_ptr(), bptr, c.data_ptr(), stream.cuda_stream)
 
+    band_plan = fi.Plan(strategy_for(fi, wl, shard.m_local, n, k), device=dev.index) if transport == "fused" else None
+    ready = torch.zeros(world, device=dev, dtype=torch.int32)
+    epoch = [0]
+
     def step():
-        if transport == "direct":
+        if transport == "fused":
+            epoch[0] += 1
+            sharded_step_fused(shard, A, Bl, Bf, C, band_plan, dist, pg, ready, epoch[0])
+        elif transport == "direct":
             sharded_step_direct(shard, A, Bl, Bf, C, gemm_ptr, dist, pg)
         elif pg is not None:
             sharded_step_peer(shard, A, Bl, Bf, C, gemm, dist, pg)
@@ -375,7 +384,10 @@ def ours_multi(args, fi, torch, rank, world):
                 "vs_baseline": None, "dtype": wl["ab"] + " in / f32 acc", "data": "synthetic (uniform on device)",
                 "config": {"workload": wl["name"], "m": m, "n": n, "k": k, "parallelism": f"mn-shard{world}",
                            "shard": f"{shard.m_local}x{n} rows of C per GPU, B chunks of {shard.n_chunk} columns",
-                           "comm": {"peer": "copy-engine pulls of B chunks from IPC-mapped peer buffers, "
+                           "comm": {"fused": "copy-engine pulls of B chunks from IPC-mapped peer buffers in "
+                                             "rotated order, each releasing a ready flag to ONE gated persistent "
+                                             "GEMM over the whole C band (tiles wait per chunk)",
+                                    "peer": "copy-engine pulls of B chunks from IPC-mapped peer buffers, "
                                             "overlapped with chunk GEMMs",
                                     "direct": "chunk GEMMs read B over NVLink from the owners' IPC-mapped buffers",
                                     }.get(transport, "NCCL per-owner broadcasts of B chunks, overlapped with chunk GEMMs"),
@@ -391,7 +403,8 @@ def ours_multi(args, fi, torch, rank, world):
                         "steps": e2e_steps,
                         "api": "dist.sharded_step* per rank with pinned host shards (A band, own B chunk "
                                "up; C band down), wall clock, max over ranks"},
-                "gpu_launches": args.steps * world * world,  # one chunk GEMM per B chunk per rank per step
+                # fused: one GEMM per rank per step; else one chunk GEMM per B chunk per rank per step
+                "gpu_launches": args.steps * world * (1 if transport == "fused" else world),
                 "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)
     if pg is not None:

@@ -115,6 +115,10 @@ public:
 
     // device buffers in the root element types and layouts; stream-ordered
     void launch(const void* dA, const void* dB, void* dC, void* stream) const;
+    // tensor-core plans: B column chunks of chunk_cols gated by ready[j] >= epoch
+    // (fi_plan_launch_gated), tile schedule starting at chunk first_chunk
+    void launch_gated(const void* dA, const void* dB, void* dC, void* stream, const unsigned* ready,
+                      unsigned epoch, long chunk_cols, int first_chunk) const;
     // anvil::run semantics on host fp32 matrices (grid snapping on ingestion)
     RunResult run_host(const Matrix& a, const Matrix* b, void* stream = nullptr) const;
     // Same on raw host fp32 arrays in the root physical layouts (extent

@@ -85,6 +85,17 @@ fi_status fi_plan_create(const char* script_utf8, int64_t m, int64_t n, int64_t 
  * reference zero-initialises the root C, sim.hpp:222-223). */
 fi_status fi_plan_launch(fi_plan plan, const void* dA, const void* dB, void* dC, void* cuda_stream);
 
+/* Gated launch of a tensor-core plan (the B all-gather of configs[4] fused into
+ * ONE persistent GEMM): B's columns are split into chunks of chunk_cols; a
+ * tile of chunk j is loaded only once ready_flags[j] >= epoch (written by
+ * fi_stream_write_u32 on the stream that copied chunk j in), and the tile
+ * schedule starts at chunk first_chunk. A chunk that never arrives traps the
+ * kernel after 4 s instead of hanging it. Not an anvil entry point: it
+ * serves the multi-GPU driver (paper_2003_06324_b200/dist.py). */
+fi_status fi_plan_launch_gated(fi_plan plan, const void* dA, const void* dB, void* dC, void* cuda_stream,
+                               const uint32_t* ready_flags, uint32_t epoch, int64_t chunk_cols,
+                               int32_t first_chunk);
+
 /* anvil::run equivalent (sim.hpp:495): host fp32 matrices in the root layouts
  * (F16/BF16 roots are snapped to their grid on ingestion, sim.hpp:507-510),
  * copies in, executes, copies the fp32 result out, synchronous. */
@@ -148,6 +159,11 @@ fi_status fi_ipc_export(const void* dptr, void* handle_out, int64_t* offset_out)
 fi_status fi_ipc_open(const void* handle, int64_t offset, void** dptr_out);
 fi_status fi_ipc_close(void* dptr, int64_t offset);
 fi_status fi_copy_async(void* dst, const void* src, int64_t bytes, void* cuda_stream);
+/* Stream-ordered 32-bit store of `value` to device address dptr, after all
+ * earlier work on the stream with a memory barrier (cuStreamWriteValue32):
+ * executed by the stream's front end, no SM -- so it can signal a persistent
+ * kernel that occupies every SM. */
+fi_status fi_stream_write_u32(void* dptr, uint32_t value, void* cuda_stream);
 
 /* Raw tensor-core GEMM entry (the kernel family behind FI_KIND_TCGEN05):
  * C = A*B, lda/ldb/ldc are physical leading dimensions in elements. */

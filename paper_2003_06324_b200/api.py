@@ -163,6 +163,15 @@ class Plan:
         N.check(N.lib.fi_plan_launch(self._h, C.c_void_p(dA), C.c_void_p(dB or 0) if dB else None,
                                      C.c_void_p(dC), C.c_void_p(stream) if stream else None))
 
+    def launch_gated(self, dA: int, dB: int, dC: int, stream: int, ready: int, epoch: int, chunk_cols: int,
+                     first_chunk: int) -> None:
+        """Launch with B's column chunks (chunk_cols wide) gated by the device
+        flags ready[j] >= epoch, scheduling chunk first_chunk first (the fused
+        all-gather -> GEMM of the multi-GPU driver)."""
+        N.check(N.lib.fi_plan_launch_gated(self._h, C.c_void_p(dA), C.c_void_p(dB), C.c_void_p(dC),
+                                           C.c_void_p(stream) if stream else None, C.c_void_p(ready),
+                                           C.c_uint32(epoch), C.c_int64(chunk_cols), C.c_int32(first_chunk)))
+
     def run_host(self, A: np.ndarray, B: Optional[np.ndarray] = None) -> np.ndarray:
         """anvil::run semantics: logical fp32 matrices in, logical fp32 C out.
 

@@ -80,6 +80,17 @@ fi_status fi_plan_launch(fi_plan plan, const void* dA, const void* dB, void* dC,
     });
 }
 
+fi_status fi_plan_launch_gated(fi_plan plan, const void* dA, const void* dB, void* dC, void* cuda_stream,
+                               const uint32_t* ready_flags, uint32_t epoch, int64_t chunk_cols,
+                               int32_t first_chunk) {
+    if (!plan || !dA || !dB || !dC || !ready_flags)
+        return rt::set_error(FI_ERR_ARGUMENT, "fi_plan_launch_gated: null argument");
+    return guarded([&] {
+        plan->plan->launch_gated(dA, dB, dC, cuda_stream, ready_flags, epoch, chunk_cols, first_chunk);
+        return FI_OK;
+    });
+}
+
 fi_status fi_plan_run_host(fi_plan plan, const float* A, const float* B, float* C) {
     if (!plan || !A || !C) return rt::set_error(FI_ERR_ARGUMENT, "fi_plan_run_host: null argument");
     return guarded([&] {

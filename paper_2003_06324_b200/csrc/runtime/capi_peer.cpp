@@ -74,3 +74,21 @@ extern "C" fi_status fi_copy_async(void* dst, const void* src, int64_t bytes, vo
                                     static_cast<cudaStream_t>(cuda_stream));
     return e == cudaSuccess ? FI_OK : cuda_err("cudaMemcpyAsync", e);
 }
+
+extern "C" fi_status fi_stream_write_u32(void* dptr, uint32_t value, void* cuda_stream) {
+    if (!dptr) return rt::set_error(FI_ERR_ARGUMENT, "fi_stream_write_u32: null address");
+    using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+    static WriteFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<WriteFn>(nullptr);
+        return reinterpret_cast<WriteFn>(p);
+    }();
+    if (!fn) return rt::set_error(FI_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+    // default flags: the write is ordered after earlier work on the stream, behind a memory barrier
+    const CUresult r = fn(static_cast<CUstream>(cuda_stream), reinterpret_cast<CUdeviceptr>(dptr), value, 0);
+    if (r != CUDA_SUCCESS) return rt::set_error(FI_ERR_CUDA, "cuStreamWriteValue32 failed (" + std::to_string(r) + ")");
+    return FI_OK;
+}

@@ -695,6 +695,30 @@ std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const 
     return std::shared_ptr<Plan>(new Plan(std::move(impl)));
 }
 
+void Plan::launch_gated(const void* dA, const void* dB, void* dC, void* stream, const unsigned* ready,
+                        unsigned epoch, long chunk_cols, int first_chunk) const {
+    const Impl& I = *impl_;
+    if (I.info.kind != 1) throw BackendError(103, "gated launches need a tensor-core (tcgen05) plan");
+    if (!ready || chunk_cols <= 0 || I.tp.N % chunk_cols != 0 || first_chunk < 0 ||
+        first_chunk >= I.tp.N / chunk_cols)
+        throw BackendError(104, "gated launch: chunk_cols must divide N, first_chunk in range, flags non-null");
+    sm100::TcGemmProblem p = I.tp;
+    p.workspace = &I.ws;
+    p.A = dA;
+    p.B = dB;
+    p.C = dC;
+    if ((reinterpret_cast<uintptr_t>(dA) | reinterpret_cast<uintptr_t>(dB)) & 15)
+        throw BackendError(104, "TMA operands must be 16-byte aligned");
+    p.b_ready = ready;
+    p.b_epoch = epoch;
+    p.b_chunk_n = chunk_cols;
+    p.b_first_chunk = first_chunk;
+    const int r = sm100::tc_gemm_launch(I.tc, p, static_cast<cudaStream_t>(stream));
+    if (r == sm100::kTcErrShape)
+        throw BackendError(104, "gated launch: chunk_cols must be a multiple of the scheduled tile width");
+    if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+}
+
 void Plan::launch(const void* dA, const void* dB, void* dC, void* stream) const {
     const Impl& I = *impl_;
     auto s = static_cast<cudaStream_t>(stream);

@@ -114,6 +114,15 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     args.out_type = cfg.out_type;
     args.group_m = cfg.group_m > 0 ? cfg.group_m : 8;
     args.tile_order = p.tile_order;
+    if (p.b_ready) {
+        const long unit_n = static_cast<long>(S::BN_TILE) * kMcast;
+        if (p.tile_order || p.b_chunk_n <= 0 || p.b_chunk_n % unit_n != 0 || p.N % p.b_chunk_n != 0)
+            return kTcErrShape;
+        args.b_ready = p.b_ready;
+        args.b_epoch = p.b_epoch;
+        args.b_chunk_tiles = static_cast<int>(p.b_chunk_n / unit_n);
+        args.n_rot = (p.b_first_chunk * args.b_chunk_tiles) % args.tiles_n;
+    }
     args.stages = cfg.stages;
     args.c_tma = c_tma ? 1 : 0;
     static const bool ring_drain_env = [] {

@@ -94,6 +94,19 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+
+// Gated B (fused all-gather): spin until tile column tn's chunk is flagged
+// ready. Out of line: the producer's loop keeps its code shape when ungated.
+__device__ __noinline__ void wait_b_chunk(const unsigned* f, unsigned epoch) {
+    if (ld_acquire_gpu(f) < epoch) {
+        const unsigned long long t0 = global_timer_ns();
+        while (ld_acquire_gpu(f) < epoch) {
+            __nanosleep(256);
+            if (global_timer_ns() - t0 > 4000000000ull) __trap();  // a lost chunk: fail, not hang
+        }
+    }
+    fence_proxy_async_global();  // copy-engine writes before the TMA reads
+}
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -208,6 +221,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     mbar_wait_cluster(rempty_bar, (static_cast<uint32_t>(it) & 1) ^ 1);
                     fence_proxy_async();
                 }
+                if (args.b_ready)  // gated B: the tile's column chunk has landed
+                    wait_b_chunk(args.b_ready + tn / args.b_chunk_tiles, args.b_epoch);
                 trace_stamp(args, it, 0);
                 ++it;
                 const int m0 = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;

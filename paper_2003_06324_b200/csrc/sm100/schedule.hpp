@@ -29,6 +29,14 @@ struct GemmArgs {
     int group_m = 8;            // raster band (tile rows) for the default order
     int stages = 0;             // pipeline depth actually used (0 = deepest that fits)
     const int* tile_order = nullptr;  // optional permutation: Fireiron block-swizzle table
+    // gated B (all-gather fused into one launch): column chunk j of B -- b_chunk_tiles
+    // scheduled tile columns -- may be read once b_ready[j] >= b_epoch (set by the
+    // copy engine's stream after the chunk has landed); the raster starts at tile
+    // column n_rot so the locally owned chunk comes first
+    const unsigned* b_ready = nullptr;
+    unsigned b_epoch = 0;
+    int b_chunk_tiles = 0;
+    int n_rot = 0;
     // stream-K
     int streamk = 0;
     int sk_tile_begin = 0;           // tiles before this index run data-parallel
@@ -131,7 +139,8 @@ FI_HD inline void tile_coords(const GemmArgs& a, int t, int& tm, int& tn) {
     int rows = a.tiles_m - g * a.group_m;
     if (rows > a.group_m) rows = a.group_m;
     tm = g * a.group_m + local % rows;
-    tn = local / rows;
+    tn = local / rows + a.n_rot;
+    if (tn >= a.tiles_n) tn -= a.tiles_n;
 }
 
 // One work unit: K-blocks [k0, k1) of columns [n_off, n_off + width) of tile `tile`.

@@ -45,6 +45,12 @@ struct TcGemmProblem {
     // stream-K partial workspace; null = a library-owned pool. Launches that
     // share a workspace must be ordered on one stream.
     TcWorkspace* workspace = nullptr;
+    // gated B (fused all-gather): B's column chunks of b_chunk_n columns become
+    // readable when b_ready[j] >= b_epoch; the schedule starts at chunk b_first_chunk
+    const unsigned* b_ready = nullptr;
+    unsigned b_epoch = 0;
+    long b_chunk_n = 0;
+    int b_first_chunk = 0;
 };
 
 // Device workspace of the stream-K fixup: one fp32 partial tile per CTA

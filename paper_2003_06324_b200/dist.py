@@ -52,8 +52,10 @@ class Shard:
         return j * self.m_local * self.n_chunk
 
     def order(self) -> List[int]:
-        """Chunk compute order: own chunk first, then the others as they land."""
-        return [self.rank] + [j for j in range(self.world) if j != self.rank]
+        """Chunk compute order: own chunk first, then the others rotated (rank
+        r pulls from r+1 first, so no owner is every rank's first source; the
+        fused GEMM's tile raster starts at chunk r and wraps the same way)."""
+        return [(self.rank + i) % self.world for i in range(self.world)]
 
 
 def make_shard(m: int, n: int, k: int, world: int, rank: int, tile_m: int = 256, tile_n: int = 256) -> Shard:
@@ -122,6 +124,7 @@ class PeerGather:
             self.peer[j] = (p.value, o)
         dev = b_full.device
         self.streams = {j: torch.cuda.Stream(device=dev) for j in self.peer}
+        self.seq_stream = torch.cuda.Stream(device=dev)  # sharded_step_fused: pulls in rotated order
         self.events = {j: torch.cuda.Event() for j in self.peer}
         self.esize = b_full.element_size()
 
@@ -161,6 +164,42 @@ def sharded_step_peer(shard: Shard, a_local, b_local, b_full, c_local, gemm: Cal
         bo, co = shard.b_chunk_offset(j), shard.c_chunk_offset(j)
         gemm(j, a_local, b_full[bo:bo + shard.b_chunk_elems],
              c_local[co:co + shard.m_local * shard.n_chunk])
+
+
+def sharded_step_fused(shard: Shard, a_local, b_local, b_full, c_local, plan, dist, pg: PeerGather, ready,
+                       epoch: int):
+    """One step as ONE persistent GEMM over this rank's whole C band with the
+    B all-gather fused in: copy engines pull the peers' chunks in rotated
+    order on one stream (sequential, so chunk i lands after i chunk-times
+    instead of all of them at the end), each followed by a stream-ordered
+    write of its ready flag (fi_stream_write_u32: no SM needed, the GEMM holds
+    them all); the GEMM starts on my own chunk and each tile's producer waits
+    for its chunk's flag before its first TMA load (fi_plan_launch_gated).
+    `plan` covers (m_local x N x K); `ready` is a device int32[world] buffer
+    whose entries only ever increase (epoch = 1, 2, ... per step)."""
+    import torch
+    me = shard.rank
+    off = shard.b_chunk_offset(me)
+    cur = torch.cuda.current_stream()
+    b_full[off:off + shard.b_chunk_elems].copy_(b_local)
+    cur.synchronize()
+    dist.barrier()  # every owner's chunk in place; every peer's pulls of the previous step done
+    N, C = pg.N, pg.C
+    rp = ready.data_ptr()
+    N.check(N.lib.fi_stream_write_u32(C.c_void_p(rp + 4 * me), C.c_uint32(epoch), C.c_void_p(cur.cuda_stream)))
+    s = pg.seq_stream
+    s.wait_stream(cur)
+    for j in shard.order():
+        if j == me:
+            continue
+        p, _ = pg.peer[j]
+        o = shard.b_chunk_offset(j) * pg.esize
+        N.check(N.lib.fi_copy_async(C.c_void_p(b_full.data_ptr() + o), C.c_void_p(p + o),
+                                    shard.b_chunk_elems * pg.esize, C.c_void_p(s.cuda_stream)))
+        N.check(N.lib.fi_stream_write_u32(C.c_void_p(rp + 4 * j), C.c_uint32(epoch), C.c_void_p(s.cuda_stream)))
+    plan.launch_gated(a_local.data_ptr(), b_full.data_ptr(), c_local.data_ptr(), cur.cuda_stream, rp, epoch,
+                      shard.n_chunk, me)
+    cur.wait_stream(s)  # the next step's barrier then also covers these pulls
 
 
 def sharded_step_direct(shard: Shard, a_local, b_local, b_full, c_local, gemm_ptr: Callable, dist, pg: PeerGather):

@@ -2,8 +2,10 @@
 share the one GPU of this environment (gloo for the process group), each
 computes its C row band with the B chunks gathered either by per-owner
 broadcasts, by copy-engine pulls from the peers' IPC-mapped buffers
-(PeerGather, the GPU driver's default), or not at all (the chunk GEMM's TMA
-reads the owner's buffer through its IPC mapping), overlapped with chunk GEMMs. Integer
+(PeerGather), or not at all (the chunk GEMM's TMA reads the owner's buffer
+through its IPC mapping), overlapped with chunk GEMMs -- or, fused (the GPU
+driver's default), by sequential copy-engine pulls that release per-chunk
+ready flags to ONE gated persistent GEMM over the whole band. Integer
 inputs: every rank's band must equal the fp64 oracle exactly, two steps in a
 row (the second re-gathers into buffers the first step read)."""
 import os
@@ -32,7 +34,7 @@ def _worker(rank, world, port, q, transport="broadcast"):
     import oracle
     import paper_2003_06324_b200 as fi
     from paper_2003_06324_b200.dist import (PeerGather, make_shard, sharded_step, sharded_step_direct,
-                                            sharded_step_peer)
+                                            sharded_step_fused, sharded_step_peer)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     m, n, k = 1024, 1024, 512
@@ -55,14 +57,18 @@ def _worker(rank, world, port, q, transport="broadcast"):
 
     want = oracle.gemm_f64(a[rank * sh.m_local:(rank + 1) * sh.m_local], b)
     ok = True
-    pg = PeerGather(sh, b_f, dist) if transport in ("peer", "direct") else None
+    pg = PeerGather(sh, b_f, dist) if transport in ("peer", "direct", "fused") else None
+    band_plan = fi.Plan(fi.strategies.tc_strategy(sh.m_local, n, k)) if transport == "fused" else None
+    ready = torch.zeros(2, device=dev, dtype=torch.int32)
 
     def gemm_ptr(j, aa, bptr, cc):
         plan.launch(aa.data_ptr(), bptr, cc.data_ptr(), stream.cuda_stream)
 
-    for _ in range(2):
+    for step in range(2):
         c_r.fill_(float("nan"))
-        if transport == "direct":
+        if transport == "fused":
+            sharded_step_fused(sh, a_r, b_l, b_f, c_r, band_plan, dist, pg, ready, step + 1)
+        elif transport == "direct":
             sharded_step_direct(sh, a_r, b_l, b_f, c_r, gemm_ptr, dist, pg)
         elif pg is not None:
             sharded_step_peer(sh, a_r, b_l, b_f, c_r, gemm, dist, pg)
@@ -78,7 +84,7 @@ def _worker(rank, world, port, q, transport="broadcast"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("transport", ["broadcast", "peer", "direct"])
+@pytest.mark.parametrize("transport", ["broadcast", "peer", "direct", "fused"])
 def test_sharded_gemm_two_ranks_one_gpu(transport):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
