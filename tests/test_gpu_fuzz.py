@@ -71,3 +71,37 @@ def test_random_tcgen05_strategy(fi, oracle, case):
     if kw["c"] != "f32":
         want = oracle.round_elem(want, kw["c"])
     assert np.array_equal(c[rows, cols], want), (m, n, k, kw)
+
+
+GATED = []
+_rg = np.random.default_rng(20261018)
+while len(GATED) < 16:
+    m, n, k, kw = draw(_rg)
+    if kw.get("split_k", 1) > 1:
+        continue
+    unit = kw["tile_n"] * (2 if kw.get("multicast") else 1)  # N columns of one scheduled unit
+    chunks = [c for c in range(1, n // unit + 1) if (n // unit) % c == 0]
+    nch = int(_rg.choice(chunks))
+    GATED.append((m, n, k, kw, n // nch, int(_rg.integers(0, nch))))
+
+
+@pytest.mark.parametrize("case", range(len(GATED)))
+def test_random_gated_launch(fi, oracle, case):
+    """Gated launches (the fused all-gather's GEMM) over random strategies,
+    chunk widths and first chunks, every flag already at the epoch: exact."""
+    import torch
+    m, n, k, kw, chunk_cols, first = GATED[case]
+    kw = dict(kw, c="f32", layouts=("colmajor", "colmajor", "colmajor"))
+    plan = fi.Plan(fi.strategies.tc_strategy(m, n, k, **kw))
+    a = oracle.fill(m, k, 300 + case, True)
+    b = oracle.fill(k, n, 400 + case, True)
+    dt = torch.bfloat16 if kw.get("ab") == "bf16" else torch.float16
+    dA = torch.from_numpy(np.ascontiguousarray(a.T).ravel()).cuda().to(dt)
+    dB = torch.from_numpy(np.asfortranarray(b).ravel(order="F").copy()).cuda().to(dt)
+    dC = torch.full((m * n,), float("nan"), device="cuda")
+    ready = torch.full((n // chunk_cols,), 3, device="cuda", dtype=torch.int32)
+    plan.launch_gated(dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), torch.cuda.current_stream().cuda_stream,
+                      ready.data_ptr(), 3, chunk_cols, first)
+    torch.cuda.synchronize()
+    c = dC.cpu().numpy().reshape(n, m).T
+    assert np.array_equal(c, oracle.gemm_f64(a, b)), (m, n, k, kw, chunk_cols, first)
