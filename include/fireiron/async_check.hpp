@@ -41,6 +41,7 @@ enum AsyncMutation : int {
     kMutUnpackedPeerStaging = 6,    // owners stage peers at j*nown chunks (the pre-remainder layout)
     kMutTxUndercount = 7,           // expect_tx without the second B half of an N-half tile
     kMutMcastSingleRelease = 8,     // multicast: a stage refilled after one pair's release, not both
+    kMutGateSkipAcquire = 9,        // gated B: the producer loads a chunk without acquiring its ready flag
 };
 
 struct AsyncCheckOptions {
@@ -53,6 +54,8 @@ struct AsyncCheckOptions {
     int pull_d = -2;              // as FI_TC_PULL_D: -2 the launcher's default, -1 no pull fixup
     int head = 1;                 // as FI_TC_HEAD: 2-slice pull tails run before the data-parallel tiles
     int mutation = kMutNone;
+    int gated_chunks = 0;         // > 0: a gated launch (fi_plan_launch_gated) with B in this many column chunks,
+    int gated_first = 0;          //      each written by a copy engine and released by its ready flag
 };
 
 struct AsyncRecord {
@@ -68,6 +71,7 @@ struct AsyncReport {
     long races = 0, capacity_errors = 0, coverage_errors = 0, deadlocks = 0;
     // the schedule that was checked
     int clusters = 0, cluster_size = 1, mode = 0, slices = 1, remainder = 0, pull = 0, head = 0, split_k = 1, stages = 0;
+    int gated_chunks = 0;  // > 0: a gated launch was modelled (B in this many copy-engine chunks)
     long units = 0, tiles = 0;
     std::vector<AsyncRecord> records;  // first 256
     bool ok() const { return races == 0 && capacity_errors == 0 && coverage_errors == 0 && deadlocks == 0; }

@@ -133,6 +133,8 @@ typedef struct fi_async_check_options {
     int32_t mutation;            /* fault injection for self-tests (0 = none)     */
     int32_t pull_d;              /* 2-slice pull fixup: -2 launcher default, -1 off */
     int32_t head;                /* pull-fixup tails before data-parallel tiles (1) */
+    int32_t gated_chunks;        /* > 0: model fi_plan_launch_gated with B in this many chunks */
+    int32_t gated_first;         /* its first chunk                                */
 } fi_async_check_options;
 int64_t fi_script_check_async(const char* script_utf8, int64_t m, int64_t n, int64_t k,
                               const fi_async_check_options* opts, char* buf, int64_t cap);

@@ -64,7 +64,8 @@ class PlanInfo(C.Structure):
 class AsyncCheckOptions(C.Structure):
     _fields_ = [("num_sms", C.c_int32), ("max_active_clusters", C.c_int32), ("streamk", C.c_int32),
                 ("remainder", C.c_int32), ("c_tma", C.c_int32), ("ring_drain", C.c_int32),
-                ("mutation", C.c_int32), ("pull_d", C.c_int32), ("head", C.c_int32)]
+                ("mutation", C.c_int32), ("pull_d", C.c_int32), ("head", C.c_int32),
+                ("gated_chunks", C.c_int32), ("gated_first", C.c_int32)]
 
 
 def _load() -> C.CDLL:

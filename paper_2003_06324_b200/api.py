@@ -63,7 +63,7 @@ def plan_summary(script: str, m: int = 0, n: int = 0, k: int = 0) -> str:
 
 MUTATIONS = {"none": 0, "skip_empty_wait": 1, "ring_drain_every_unit": 2, "flag_before_bulk_wait": 3,
              "skip_tmem_empty_wait": 4, "remainder_slot_collision": 5, "unpacked_peer_staging": 6,
-             "tx_undercount": 7, "mcast_single_release": 8}
+             "tx_undercount": 7, "mcast_single_release": 8, "gate_skip_acquire": 9}
 
 
 class AsyncReport:
@@ -95,13 +95,16 @@ class AsyncReport:
 
 def check_async(script: str, m: int = 0, n: int = 0, k: int = 0, *, num_sms: int = 148,
                 max_active_clusters: int = 0, streamk: int = -1, remainder: int = 1, c_tma: int = -1,
-                ring_drain: int = 1, pull_d: int = -2, head: int = 1, mutation: str = "none") -> AsyncReport:
+                ring_drain: int = 1, pull_d: int = -2, head: int = 1, mutation: str = "none",
+                gated_chunks: int = 0, gated_first: int = 0) -> AsyncReport:
     """CPU check of the asynchronous protocol (mbarrier phases, TMA, tcgen05
     commits, TMEM hand-off, bulk copies, epoch flags) of the launch a tcgen05
     strategy lowers to: races, capacity, coverage, deadlock
-    (include/fireiron/async_check.hpp). No GPU needed."""
+    (include/fireiron/async_check.hpp). No GPU needed. gated_chunks > 0 models
+    a gated launch (fi_plan_launch_gated): B in that many column chunks, each
+    landed by a copy engine and released by its ready flag."""
     o = N.AsyncCheckOptions(num_sms, max_active_clusters, streamk, remainder, c_tma, ring_drain,
-                            MUTATIONS[mutation], pull_d, head)
+                            MUTATIONS[mutation], pull_d, head, gated_chunks, gated_first)
     return AsyncReport(_text(N.lib.fi_script_check_async, _enc(script), m, n, k, C.byref(o)))
 
 

@@ -39,7 +39,8 @@ std::string AsyncReport::to_string() const {
        << "  schedule: " << clusters << " clusters x " << cluster_size << " CTAs, " << tiles << " tiles, " << units
        << " units, mode " << mode << ", slices " << slices << (remainder ? " + remainder" : "")
        << (pull ? (head ? " (pull fixup, first)" : " (pull fixup)") : "") << ", split-k "
-       << split_k << ", stages " << stages << "\n"
+       << split_k << ", stages " << stages
+       << (gated_chunks ? ", B gated in " + std::to_string(gated_chunks) + " copy-engine chunks" : std::string()) << "\n"
        << "  events " << events << ", races " << races << ", capacity " << capacity_errors << ", coverage "
        << coverage_errors << ", deadlocks " << deadlocks << "\n";
     for (const auto& r : records)
@@ -81,7 +82,7 @@ void join(Clock& dst, const Clock& src) {
         if (src[i] > dst[i]) dst[i] = src[i];
 }
 
-enum Space : uint64_t { kRing = 1, kEpi, kTmem, kWs, kC };
+enum Space : uint64_t { kRing = 1, kEpi, kTmem, kWs, kC, kB };
 const char* space_name(uint64_t s) {
     switch (s) {
         case kRing: return "ring";
@@ -89,6 +90,7 @@ const char* space_name(uint64_t s) {
         case kTmem: return "tmem";
         case kWs: return "workspace";
         case kC: return "C";
+        case kB: return "B chunk";
     }
     return "?";
 }
@@ -135,7 +137,8 @@ public:
     Checker(const GemmArgs& args, int clusters, long slots, const AsyncCheckOptions& o, AsyncReport& rep)
         : a_(args), ncl_(clusters), slots_(slots), opt_(o), rep_(rep) {
         nctas_ = ncl_ * kRanks;
-        nagents_ = nctas_ * kRoles;
+        nagents_ = nctas_ * kRoles + 1;  // + the copy engine that lands gated B chunks
+        ce_ = nagents_ - 1;
         vc_.assign(static_cast<size_t>(nagents_), Clock(static_cast<size_t>(nagents_), 0));
         ctas_.resize(static_cast<size_t>(nctas_));
         for (auto& c : ctas_) {
@@ -157,6 +160,16 @@ public:
     }
 
     void run() {
+        if (opt_.gated_chunks > 0) {  // the copy engine lands chunk j, then its stream writes flag j
+            b_flags_.resize(static_cast<size_t>(opt_.gated_chunks));
+            for (int i = 0; i < opt_.gated_chunks; ++i) {
+                const int j = (opt_.gated_first + i) % opt_.gated_chunks;
+                access(ce_, kB, 0, static_cast<uint64_t>(j), true);
+                ++vc_[static_cast<size_t>(ce_)][static_cast<size_t>(ce_)];
+                b_flags_[static_cast<size_t>(j)].value = a_.epoch;
+                b_flags_[static_cast<size_t>(j)].clock = vc_[static_cast<size_t>(ce_)];
+            }
+        }
         std::vector<Task> tasks;
         for (int c = 0; c < ncl_; ++c)
             for (int r = 0; r < kRanks; ++r) {
@@ -225,6 +238,8 @@ private:
     std::unordered_map<long, int> stores_;  // (tile*NCH_ALL + chunk) -> times stored
 
     int agent(int cta, int role) const { return cta * kRoles + role; }
+    int ce_ = 0;
+    std::vector<Flag> b_flags_;  // gated B: ready flag of each column chunk
     int cta_of(int c, int r) const { return c * kRanks + r; }
 
     void init_bar(Barrier& b, int count) {
@@ -238,6 +253,7 @@ private:
         if (rep_.records.size() < 256) rep_.records.push_back({kind, res, index, std::move(first), std::move(second), cluster});
     }
     std::string who(int ag) const {
+        if (ag == ce_) return "copy-engine";
         return std::string(role_name(ag % kRoles)) + "@cta" + std::to_string(ag / kRoles);
     }
 
@@ -399,6 +415,15 @@ private:
                                     ? S::A_BYTES + static_cast<long>(b_rows) * S::BK * 2  // the first N-half kernel's bug
                                     : S::stage_tx_bytes(b_rows) / kCtaGroup;
             const long a_bytes = S::A_BYTES, b_bytes = static_cast<long>(b_rows) * S::BK * 2 * kNHalves;
+            int chunk = -1;  // gated B: wait_b_chunk (ld.acquire of the chunk's ready flag) before the loads
+            if (!b_flags_.empty()) {
+                int tm, tn;
+                tile_coords(a_, u.tile, tm, tn);
+                chunk = tn / a_.b_chunk_tiles;
+                Flag& f = b_flags_[static_cast<size_t>(chunk)];
+                co_await WaitUntil{[&f, this] { return f.value >= a_.epoch; }};
+                if (opt_.mutation != kMutGateSkipAcquire) join(vc_[static_cast<size_t>(P)], f.clock);
+            }
             for (int kb = u.k0; kb < u.k1; ++kb) {
                 if (opt_.mutation != kMutSkipEmptyWait) {
                     co_await wait(C.empty[static_cast<size_t>(s)], ph ^ 1);
@@ -422,6 +447,7 @@ private:
                     smem(T, cta, kRing, st, a_bytes, true);  // A slab(s)
                     complete_tx(full, a_bytes, vc_[static_cast<size_t>(T)], lap);
                 }
+                if (chunk >= 0) access(T, kB, 0, static_cast<uint64_t>(chunk), false);  // TMA reads the landed chunk
                 smem(T, cta, kRing, st + S::A_BYTES, b_bytes, true);  // B half (halves)
                 complete_tx(full, b_bytes, vc_[static_cast<size_t>(T)], lap);
                 if (++s == nst_) {
@@ -762,6 +788,17 @@ void run_checker(GemmArgs args, int sms, int force_slices, const AsyncCheckOptio
         args.sk_head = plan.sk_head;
     }
     args.epoch = 1;
+    if (o.gated_chunks > 0) {  // as fi_plan_launch_gated: chunk tiles, raster rotated to the first chunk
+        if (args.tiles_n % o.gated_chunks != 0 || o.gated_first < 0 || o.gated_first >= o.gated_chunks) {
+            ++rep.capacity_errors;
+            rep.records.push_back({"capacity", "B chunk", o.gated_chunks, "chunks must split the tile columns evenly", "", -1});
+            return;
+        }
+        args.b_chunk_tiles = args.tiles_n / o.gated_chunks;
+        rep.gated_chunks = o.gated_chunks;
+        args.n_rot = o.gated_first * args.b_chunk_tiles;
+        args.b_epoch = 1;
+    }
     rep.clusters = plan.clusters;
     rep.mode = plan.mode;
     rep.slices = plan.slices;

@@ -195,6 +195,8 @@ int64_t fi_script_check_async(const char* script_utf8, int64_t m, int64_t n, int
             o.mutation = opts->mutation;
             o.pull_d = opts->pull_d;
             o.head = opts->head;
+            o.gated_chunks = opts->gated_chunks;
+            o.gated_first = opts->gated_first;
         }
         return check_async(ps.root, ps.tree, o, ps.micro_kernels).to_string();
     });

@@ -30,13 +30,14 @@ struct Args {
     bool float_mode = false, dump_trace = false;
     double tolerance = -1.0;
     std::string out, load_a, load_b, dump_c;
+    int gated_chunks = 0, gated_first = 0;  // check-async: model a gated launch
 };
 
 [[noreturn]] void usage() {
     std::fprintf(stderr,
                  "usage: fireiron {elaborate|codegen|simulate|verify|check-async} <script.fi> [--m M] [--n N] [--k K]\n"
                  "       [--seed S] [--float] [--load-a F] [--load-b F] [--dump-c F] [--tolerance T]\n"
-                 "       [--dump-trace] [--out F]\n");
+                 "       [--dump-trace] [--out F] [--gated-chunks C [--gated-first F]]\n");
     std::exit(2);
 }
 
@@ -62,6 +63,8 @@ Args parse_args(int argc, char** argv) {
         else if (f == "--load-a") a.load_a = val();
         else if (f == "--load-b") a.load_b = val();
         else if (f == "--dump-c") a.dump_c = val();
+        else if (f == "--gated-chunks") a.gated_chunks = std::stoi(val());
+        else if (f == "--gated-first") a.gated_first = std::stoi(val());
         else usage();
     }
     return a;
@@ -156,7 +159,10 @@ int main(int argc, char** argv) {
         }
         if (a.cmd == "check-async") {  // CPU protocol check of the tcgen05 launch (no GPU)
             ParsedScript s = load(a);
-            const AsyncReport r = check_async(s.root, s.tree, AsyncCheckOptions{}, s.micro_kernels);
+            AsyncCheckOptions o;
+            o.gated_chunks = a.gated_chunks;
+            o.gated_first = a.gated_first;
+            const AsyncReport r = check_async(s.root, s.tree, o, s.micro_kernels);
             std::cout << r.to_string();
             return r.ok() ? 0 : 1;
         }

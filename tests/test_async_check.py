@@ -103,6 +103,32 @@ def test_injected_faults_are_reported(fi, tc, mutation, shape, kw, field):
     assert getattr(bad, field) > 0, bad.text
 
 
+# ---------------------------------------------------------------- gated launches
+GATED = [  # (shape, strategy kwargs, chunks, first chunk): the fused all-gather's GEMM
+    ((2048, 16384, 1024), dict(ab="bf16", tile_m=512), 8, 3),  # C5 band at 8 GPUs, slab tiles
+    ((2048, 4096, 2048), {}, 4, 0),
+    ((1024, 2048, 512), dict(tile_n=128, multicast=True), 4, 1),
+    ((512, 1024, 4096), dict(pair=False, tile_n=128), 2, 1),   # K-slice tail units gated too
+]
+
+
+@pytest.mark.parametrize("shape,kw,chunks,first", GATED)
+def test_gated_launch_protocol(fi, tc, shape, kw, chunks, first):
+    """B chunks landed by a copy engine and released by ready flags: every TMA
+    read of a chunk must happen after the producer acquired its flag; a
+    producer that skips the acquire races the copy engine."""
+    s = tc(*shape, **kw)
+    r = fi.check_async(s, gated_chunks=chunks, gated_first=first)
+    assert r.ok, r.text
+    bad = fi.check_async(s, gated_chunks=chunks, gated_first=first, mutation="gate_skip_acquire")
+    assert bad.races > 0 and "B chunk" in bad.text
+
+
+def test_gated_chunks_must_split_the_tile_columns(fi, tc):
+    r = fi.check_async(tc(2048, 4096, 1024), gated_chunks=3)
+    assert not r.ok and r.capacity_errors > 0
+
+
 def test_non_tensor_core_tree_is_rejected(fi):
     from paper_2003_06324_b200 import FiError
     with pytest.raises(FiError):
