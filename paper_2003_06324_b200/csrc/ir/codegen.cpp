@@ -483,7 +483,9 @@ TcStrategy match_tc_strategy(const Spec& root, const NodePtr& tree, const MicroK
     }
     if (tc.mcast > 1 && (tc.tile_m != 256 || tc.tile_n > 256 || tc.split_k > 1 || root.n() % (2L * tc.tile_n)))
         return reject("multicast pairs need 256-row tiles of N <= 256, no split-K, and N a multiple of 2 tiles");
-    if ((tc.tile_m == 512 || tc.tile_n == 512) && (tc.tile_m * tc.tile_n != 512 * 256 || tc.split_k > 1))
+    if ((tc.tile_m == 512 || tc.tile_n == 512) && tc.tile_m * tc.tile_n != 512 * 256)
+        return reject("block tile M 512 needs N 256 (two A slabs sharing B), N 512 needs M 256 (two N halves sharing A)");
+    if ((tc.tile_m == 512 || tc.tile_n == 512) && tc.split_k > 1)
         return reject("512 x 256 / 256 x 512 pair tiles take no split-K (their accumulator fills TMEM)");
     if (tc.split_k > 1) {
         const int cluster = tc.split_k * tc.cta_group;
