@@ -124,7 +124,12 @@ class PeerGather:
             self.peer[j] = (p.value, o)
         dev = b_full.device
         self.streams = {j: torch.cuda.Stream(device=dev) for j in self.peer}
-        self.seq_stream = torch.cuda.Stream(device=dev)  # sharded_step_fused: pulls in rotated order
+        # sharded_step_fused: pulls in rotated order, dealt round-robin over a few
+        # streams (FI_DIST_PULL_STREAMS, default 2) so more than one copy engine
+        # can run while the chunks still land roughly in compute order
+        import os
+        n = max(1, int(os.environ.get("FI_DIST_PULL_STREAMS", "2")))
+        self.seq_streams = [torch.cuda.Stream(device=dev) for _ in range(n)]
         self.events = {j: torch.cuda.Event() for j in self.peer}
         self.esize = b_full.element_size()
 
@@ -170,10 +175,10 @@ def sharded_step_fused(shard: Shard, a_local, b_local, b_full, c_local, plan, di
                        epoch: int):
     """One step as ONE persistent GEMM over this rank's whole C band with the
     B all-gather fused in: copy engines pull the peers' chunks in rotated
-    order on one stream (sequential, so chunk i lands after i chunk-times
-    instead of all of them at the end), each followed by a stream-ordered
-    write of its ready flag (fi_stream_write_u32: no SM needed, the GEMM holds
-    them all); the GEMM starts on my own chunk and each tile's producer waits
+    order, dealt over FI_DIST_PULL_STREAMS streams (default 2) that each copy
+    sequentially -- so chunks land roughly in compute order instead of all at
+    the end -- each copy followed by a stream-ordered write of its ready flag
+    (fi_stream_write_u32: no SM needed, the GEMM holds them all); the GEMM starts on my own chunk and each tile's producer waits
     for its chunk's flag before its first TMA load (fi_plan_launch_gated).
     `plan` covers (m_local x N x K); `ready` is a device int32[world] buffer
     whose entries only ever increase (epoch = 1, 2, ... per step)."""
@@ -187,11 +192,10 @@ def sharded_step_fused(shard: Shard, a_local, b_local, b_full, c_local, plan, di
     N, C = pg.N, pg.C
     rp = ready.data_ptr()
     N.check(N.lib.fi_stream_write_u32(C.c_void_p(rp + 4 * me), C.c_uint32(epoch), C.c_void_p(cur.cuda_stream)))
-    s = pg.seq_stream
-    s.wait_stream(cur)
-    for j in shard.order():
-        if j == me:
-            continue
+    for s in pg.seq_streams:
+        s.wait_stream(cur)
+    for i, j in enumerate(x for x in shard.order() if x != me):
+        s = pg.seq_streams[i % len(pg.seq_streams)]
         p, _ = pg.peer[j]
         o = shard.b_chunk_offset(j) * pg.esize
         N.check(N.lib.fi_copy_async(C.c_void_p(b_full.data_ptr() + o), C.c_void_p(p + o),
@@ -199,7 +203,8 @@ def sharded_step_fused(shard: Shard, a_local, b_local, b_full, c_local, plan, di
         N.check(N.lib.fi_stream_write_u32(C.c_void_p(rp + 4 * j), C.c_uint32(epoch), C.c_void_p(s.cuda_stream)))
     plan.launch_gated(a_local.data_ptr(), b_full.data_ptr(), c_local.data_ptr(), cur.cuda_stream, rp, epoch,
                       shard.n_chunk, me)
-    cur.wait_stream(s)  # the next step's barrier then also covers these pulls
+    for s in pg.seq_streams:
+        cur.wait_stream(s)  # the next step's barrier then also covers these pulls
 
 
 def sharded_step_direct(shard: Shard, a_local, b_local, b_full, c_local, gemm_ptr: Callable, dist, pg: PeerGather):
