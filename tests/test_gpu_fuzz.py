@@ -3,7 +3,9 @@ pair, 512x256 slabs, 256x512 N halves, multicast pairs), tile N, split-K,
 pipeline depth, operand layouts, C element type and problem shape, drawn with
 a fixed seed. Every case must be integer-exact against the fp64 oracle at
 sampled points (C in f16/bf16: exact after rounding the oracle) and must pass
-the CPU protocol checker first."""
+the CPU protocol checker first. 80 f16 cases, 16 with bf16 operands, and 16
+gated launches (the fused all-gather's GEMM: random chunk widths and first
+chunks)."""
 import numpy as np
 import pytest
 
@@ -105,3 +107,29 @@ def test_random_gated_launch(fi, oracle, case):
     torch.cuda.synchronize()
     c = dC.cpu().numpy().reshape(n, m).T
     assert np.array_equal(c, oracle.gemm_f64(a, b)), (m, n, k, kw, chunk_cols, first)
+
+
+BF16 = []
+_rb = np.random.default_rng(20261019)
+while len(BF16) < 16:
+    BF16.append(draw(_rb))
+
+
+@pytest.mark.parametrize("case", range(len(BF16)))
+def test_random_bf16_strategy(fi, oracle, case):
+    """The same random strategy space with bf16 operands (the C5 element type)."""
+    m, n, k, kw = BF16[case]
+    kw = dict(kw, ab="bf16")
+    script = fi.strategies.tc_strategy(m, n, k, **kw)
+    chk = fi.check_async(script)
+    assert chk.ok, (kw, chk.text)
+    plan = fi.Plan(script)
+    a = oracle.fill(m, k, 500 + case, True)
+    b = oracle.fill(k, n, 600 + case, True)
+    c = plan.run_host(a, b)
+    rng = np.random.default_rng(case)
+    rows, cols = rng.integers(0, m, 2048), rng.integers(0, n, 2048)
+    want = oracle.sample_f64(oracle.round_elem(a, "bf16"), oracle.round_elem(b, "bf16"), rows, cols).astype(np.float32)
+    if kw["c"] != "f32":
+        want = oracle.round_elem(want, kw["c"])
+    assert np.array_equal(c[rows, cols], want), (m, n, k, kw)
