@@ -252,3 +252,49 @@ def test_multicast_multi_wave_uniform(fi, oracle, monkeypatch):
     c, ar, br = run(fi, oracle, s, m, n, k, False, seed=61)
     plain = fi.Plan(fi.strategies.tc_strategy(m, n, k))
     assert np.max(np.abs(plain.run_host(oracle.fill(m, k, 61, False), oracle.fill(k, n, 62, False)) - c)) <= 1e-4
+
+
+def _sampled_exact(torch, np, A_km, B_nk, C_nm, m, n, samples=1024, seed=5):
+    """C (column-major M x N, stored as [n][m]) against fp64 dot products of sampled
+    (row, col) pairs of the integer operands (A stored [k][m], B stored [n][k])."""
+    rng = np.random.default_rng(seed)
+    rows, cols = rng.integers(0, m, samples), rng.integers(0, n, samples)
+    ri, ci = torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda()
+    a = A_km[:, ri].T.float().cpu().numpy().astype(np.float64)   # samples x k
+    b = B_nk[ci, :].float().cpu().numpy().astype(np.float64)      # samples x k
+    want = np.einsum("sk,sk->s", a, b)
+    got = C_nm.view(n, m)[ci, ri].cpu().numpy().astype(np.float64)
+    return np.array_equal(got, want)
+
+
+def test_c5_full_size_sampled_exact(fi):
+    """configs[4] at full size on one GPU (16384^3 bf16, 512x256 slab tiles):
+    integer operands generated on the device, 1024 sampled outputs exact."""
+    import torch
+    m = n = k = 16384
+    plan = fi.Plan(fi.strategies.c5_strategy())
+    g = torch.Generator(device="cuda").manual_seed(7)
+    A = torch.randint(-3, 4, (k, m), device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randint(-3, 4, (n, k), device="cuda", generator=g).to(torch.bfloat16)
+    C = torch.empty(n * m, device="cuda")
+    plan.launch(A.data_ptr(), B.data_ptr(), C.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert _sampled_exact(torch, np, A, B, C, m, n)
+
+
+def test_c5_band_gated_full_size_sampled_exact(fi):
+    """The 8-GPU shard of configs[4] as the fused all-gather runs it: one gated
+    launch over a 2048 x 16384 x 16384 band, B in 8 chunks, starting at chunk 3."""
+    import torch
+    m, n, k = 2048, 16384, 16384
+    plan = fi.Plan(fi.strategies.c5_strategy(m, n, k))
+    g = torch.Generator(device="cuda").manual_seed(8)
+    A = torch.randint(-3, 4, (k, m), device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randint(-3, 4, (n, k), device="cuda", generator=g).to(torch.bfloat16)
+    C = torch.full((n * m,), float("nan"), device="cuda")
+    ready = torch.ones(8, device="cuda", dtype=torch.int32)
+    plan.launch_gated(A.data_ptr(), B.data_ptr(), C.data_ptr(), torch.cuda.current_stream().cuda_stream,
+                      ready.data_ptr(), 1, n // 8, 3)
+    torch.cuda.synchronize()
+    assert not torch.isnan(C).any().item()
+    assert _sampled_exact(torch, np, A, B, C, m, n)
