@@ -181,7 +181,11 @@ def sharded_step_fused(shard: Shard, a_local, b_local, b_full, c_local, plan, di
     (fi_stream_write_u32: no SM needed, the GEMM holds them all); the GEMM starts on my own chunk and each tile's producer waits
     for its chunk's flag before its first TMA load (fi_plan_launch_gated).
     `plan` covers (m_local x N x K); `ready` is a device int32[world] buffer
-    whose entries only ever increase (epoch = 1, 2, ... per step)."""
+    whose entries only ever increase (epoch = 1, 2, ... per step).
+    The step writes b_local into this rank's slot of b_full before the barrier,
+    while a slower peer may still be pulling that slot for the previous step:
+    harmless when the chunk does not change between steps (the benchmark); a
+    caller that changes b_local between steps must barrier before the call."""
     import torch
     me = shard.rank
     off = shard.b_chunk_offset(me)
