@@ -234,10 +234,15 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
             ws->flag_count = need_f;
             ws->epoch = 0;
         }
+        if (!ws->ctr) {
+            if (cudaMallocAsync(&ws->ctr, 2 * sizeof(unsigned), stream) != cudaSuccess) return kTcErrCuda;
+            if (cudaMemsetAsync(ws->ctr, 0, 2 * sizeof(unsigned), stream) != cudaSuccess) return kTcErrCuda;
+        }
         args.streamk = mode;
         args.workspace = ws->partials;
         args.flags = ws->flags;
         args.epoch = ++ws->epoch;
+        args.epoch_ctr = ws->ctr;
     }
     clusters = plan.clusters;
     lc.gridDim = dim3(clusters * kCluster, 1, 1);
@@ -276,6 +281,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
 TcWorkspace::~TcWorkspace() {
     if (partials) cudaFree(partials);
     if (flags) cudaFree(flags);
+    if (ctr) cudaFree(ctr);
 }
 
 TcLaunchInfo tc_gemm_last_launch() { return g_last; }

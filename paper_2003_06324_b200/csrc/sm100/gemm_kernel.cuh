@@ -348,6 +348,26 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         Unit u;
         const int kb = args.k_blocks;
         uint32_t epi_chunk = 0;  // staged C chunks so far (alternating buffers)
+        // this launch's epoch for the tail-fixup flags: the device counter + 1 when
+        // the workspace carries one (correct under CUDA-graph replay, where a
+        // host-side epoch would be frozen at capture), else the host's value. One
+        // thread reads it and counts the CTA in; the last CTA in advances the
+        // counter for the next launch -- all while the first main loop runs.
+        if (q == 0 && lane == 0) {
+            unsigned e = args.epoch;
+            if (args.epoch_ctr) {
+                e = *reinterpret_cast<volatile const unsigned*>(args.epoch_ctr) + 1u;
+                __threadfence();  // the read completes before this CTA is counted in
+                if (atomicAdd(args.epoch_ctr + 1, 1u) == gridDim.x - 1) {
+                    __threadfence();
+                    args.epoch_ctr[1] = 0;
+                    atomicAdd(args.epoch_ctr, 1u);
+                }
+            }
+            tmem_slot[1] = e;
+        }
+        epilogue_bar();
+        const unsigned epoch = tmem_slot[1];
         // TMEM -> RF -> SMEM for nch 32-column chunks into slot(c) (thread `row`
         // writes bank row % 32: conflict-free), TMEM loads double-buffered; after
         // each chunk pair one proxy fence + barrier, then one thread issues
@@ -508,7 +528,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                             bulk_wait_group<0>();
                             fence_proxy_async_global();
                             trace_stamp(args, it - 1, 4);
-                            st_release_gpu(args.flags + (u.slot * kCtaGroup + pair_rank), args.epoch);
+                            st_release_gpu(args.flags + (u.slot * kCtaGroup + pair_rank), epoch);
                         }
                         __syncwarp();
                     } else {
@@ -516,7 +536,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                         const float* peer_ws = args.workspace + static_cast<long>(ps * kCtaGroup + pair_rank) * S::WS_FLOATS;
                         const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
                         if (q == 0 && lane == 0) {
-                            while (ld_acquire_gpu(args.flags + (ps * kCtaGroup + pair_rank)) < args.epoch) __nanosleep(64);
+                            while (ld_acquire_gpu(args.flags + (ps * kCtaGroup + pair_rank)) < epoch) __nanosleep(64);
                             fence_proxy_async_global();
                             trace_stamp(args, it - 1, 4);
                             bulk_wait_group_read<0>();  // earlier units' C stores have left the epi buffers
@@ -626,14 +646,14 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                         bulk_wait_group<0>();        // my partial chunks are in global memory
                         fence_proxy_async_global();  // async-proxy writes before the release
                         trace_stamp(args, it - 1, 4);
-                        st_release_gpu(args.flags + (u.slot * kCtaGroup + pair_rank), args.epoch);
+                        st_release_gpu(args.flags + (u.slot * kCtaGroup + pair_rank), epoch);
                         if (nown > 0) {
                             mbar_arrive_expect_tx(&stage_bar[0], (nsrc - 1) * nown * kChunkBytes);
                             for (int j = 0; j < nsrc; ++j) {
                                 if (j == s) continue;
                                 const int ps = j < nslc ? tile_idx + j * rest  // slot of source j
                                                         : remainder_slot(args, rest, nclusters, tile_idx);
-                                while (ld_acquire_gpu(args.flags + (ps * kCtaGroup + pair_rank)) < args.epoch)
+                                while (ld_acquire_gpu(args.flags + (ps * kCtaGroup + pair_rank)) < epoch)
                                     __nanosleep(32);
                                 fence_proxy_async_global();
                                 bulk_copy_g2s(peer + (j < s ? j : j - 1) * nown * kChunkFloats,

@@ -64,6 +64,10 @@ struct GemmArgs {
     unsigned* flags = nullptr;       // [slots][kCtaGroup] epoch of the published partial
                                      // slots: one per cluster + sk_extra*(sk_q-1)
     unsigned epoch = 0;              // this launch's epoch (> every earlier launch's)
+    // device epoch counter [2] = {epoch, CTAs done}: when set, a launch's epoch is
+    // counter + 1, read on the device, and the last CTA to finish advances it --
+    // so a launch captured in a CUDA graph gets a fresh epoch on every replay
+    unsigned* epoch_ctr = nullptr;
     // optional timeline (FI_TC_TRACE): [cta][unit < 16][16] %globaltimer stamps
     // [0..7] and clock64 [8..15] of: producer first load, MMA last commit,
     // epilogue accumulator ready, epilogue done, tail partial published, tail

@@ -60,6 +60,7 @@ struct TcWorkspace {
     unsigned* flags = nullptr;
     size_t partial_floats = 0, flag_count = 0;
     unsigned epoch = 0;  // incremented by every launch that uses it
+    unsigned* ctr = nullptr;  // device {epoch, CTAs done}: the graph-safe epoch (GemmArgs::epoch_ctr)
     ~TcWorkspace();
 };
 
