@@ -415,7 +415,13 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
         p.N = static_cast<int>(c1 - c0);
         ck(cudaEventRecord(ev_g[2 * ng], s), "cudaEventRecord");
         const int r = sm100::tc_gemm_launch(I.tc, p, s);
-        if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+        if (r == sm100::kTcErrCapture)
+            throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
+                                    "the CUDA-graph capture");
+        if (r == sm100::kTcErrCapture)
+        throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
+                                "the CUDA-graph capture");
+    if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
         ck(cudaEventRecord(ev_g[2 * ng + 1], s), "cudaEventRecord");
         const float* result = reinterpret_cast<const float*>(base + typed_c);
         if (ec != 0) {
@@ -534,7 +540,13 @@ double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, f
         p.N = static_cast<int>(nc);
         ck(cudaEventRecord(ev_g[2 * j], s), "cudaEventRecord");
         const int r = sm100::tc_gemm_launch(I.tc, p, s);
-        if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+        if (r == sm100::kTcErrCapture)
+            throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
+                                    "the CUDA-graph capture");
+        if (r == sm100::kTcErrCapture)
+        throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
+                                "the CUDA-graph capture");
+    if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
         ck(cudaEventRecord(ev_g[2 * j + 1], s), "cudaEventRecord");
         const float* result = reinterpret_cast<const float*>(base + typed_c) + c0;
         if (ec != 0) {
@@ -716,6 +728,9 @@ void Plan::launch_gated(const void* dA, const void* dB, void* dC, void* stream, 
     const int r = sm100::tc_gemm_launch(I.tc, p, static_cast<cudaStream_t>(stream));
     if (r == sm100::kTcErrShape)
         throw BackendError(104, "gated launch: chunk_cols must be a multiple of the scheduled tile width");
+    if (r == sm100::kTcErrCapture)
+        throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
+                                "the CUDA-graph capture");
     if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
 }
 
@@ -731,7 +746,13 @@ void Plan::launch(const void* dA, const void* dB, void* dC, void* stream) const 
         if ((reinterpret_cast<uintptr_t>(dA) | reinterpret_cast<uintptr_t>(dB)) & 15)
             throw BackendError(104, "TMA operands must be 16-byte aligned");
         const int r = sm100::tc_gemm_launch(I.tc, p, s);
-        if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+        if (r == sm100::kTcErrCapture)
+            throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
+                                    "the CUDA-graph capture");
+        if (r == sm100::kTcErrCapture)
+        throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
+                                "the CUDA-graph capture");
+    if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
         return;
     }
     const BufferDecl& out = I.root(I.out_root());

@@ -216,6 +216,13 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         const size_t slots = static_cast<size_t>(plan.slots);
         const size_t need_p = slots * kCtaGroup * S::WS_FLOATS;
         const size_t need_f = slots * kCtaGroup;
+        // memory allocated while a stream is being captured would belong to the
+        // graph: the plan must have run once (outside the capture) first
+        if (ws->partial_floats < need_p || ws->flag_count < need_f || !ws->ctr) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            if (cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+                return kTcErrCapture;
+        }
         // growth is stream-ordered (cudaFreeAsync / cudaMallocAsync): a launch that
         // needs a larger workspace must not synchronise the device, e.g. inside
         // the host pipeline while uploads are still in flight

@@ -11,6 +11,7 @@ constexpr int kTcErrShape = 1;
 constexpr int kTcErrUnsupported = 2;
 constexpr int kTcErrTensorMap = 3;
 constexpr int kTcErrCuda = 4;
+constexpr int kTcErrCapture = 5;  // the workspace would be allocated inside a CUDA-graph capture
 
 struct TcGemmConfig {
     int cta_group = 2;   // 1: tcgen05 cta_group::1, M tile 128; 2: CTA pair, M tile 256

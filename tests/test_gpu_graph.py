@@ -48,3 +48,17 @@ def test_graph_replay_with_new_inputs(fi, m, n, k, kw):
         g.replay()
         torch.cuda.synchronize()
         assert _check(torch, A, B, C, m, n, trial), f"replay {trial}"
+
+
+def test_first_launch_inside_a_capture_is_refused(fi):
+    """The stream-K workspace cannot be allocated inside a capture (it would be
+    graph-owned memory): the launch fails with a clear error instead."""
+    import torch
+    plan = fi.Plan(fi.strategies.tc_strategy(4096, 4096, 4096))  # pull-fixup tail: needs a workspace
+    A = torch.zeros((4096, 4096), device="cuda", dtype=torch.float16)
+    C = torch.empty(4096 * 4096, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(fi.FiError) as e:
+        with torch.cuda.graph(g):
+            plan.launch(A.data_ptr(), A.data_ptr(), C.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert "outside" in str(e.value)
