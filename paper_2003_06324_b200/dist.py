@@ -185,7 +185,10 @@ def sharded_step_fused(shard: Shard, a_local, b_local, b_full, c_local, plan, di
     The step writes b_local into this rank's slot of b_full before the barrier,
     while a slower peer may still be pulling that slot for the previous step:
     harmless when the chunk does not change between steps (the benchmark); a
-    caller that changes b_local between steps must barrier before the call."""
+    caller that changes b_local between steps must barrier before the call.
+    The epoch is a host value written by stream memops and passed to the
+    launch, so a captured step would replay with a frozen epoch: run it
+    eagerly (the GEMM's own stream-K epoch is device-side and graph-safe)."""
     import torch
     me = shard.rank
     off = shard.b_chunk_offset(me)
