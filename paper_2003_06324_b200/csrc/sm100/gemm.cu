@@ -156,7 +156,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     lc.blockDim = dim3(S::kThreads, 1, 1);
     lc.dynamicSmemBytes = S::SMEM_BYTES;
     lc.stream = stream;
-    cudaLaunchAttribute attrs[1];
+    cudaLaunchAttribute attrs[2];
     int nattr = 0;
     if (kCluster > 1) {
         attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -262,6 +262,19 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         if (!trace_buf) cudaMalloc(&trace_buf, 148 * 16 * 16 * sizeof(unsigned long long));
         cudaMemsetAsync(trace_buf, 0, trace_n * sizeof(unsigned long long), stream);
         args.trace = trace_buf;
+    }
+    // stream-K owners spin on flags other clusters publish, so every CTA must be
+    // resident at once: a cooperative launch guarantees it even when kernels on
+    // other streams hold SMs (two concurrent stream-K launches could otherwise
+    // each wait on CTAs of their own that cannot be scheduled)
+    static const bool coop_env = [] {
+        const char* v = std::getenv("FI_TC_COOP");
+        return !(v && v[0] == '0');
+    }();
+    if (sk && coop_env) {
+        attrs[lc.numAttrs].id = cudaLaunchAttributeCooperative;
+        attrs[lc.numAttrs].val.cooperative = 1;
+        ++lc.numAttrs;
     }
     cudaError_t e = cudaLaunchKernelEx(&lc, kernel, tmA, tmB, tmB2, tmC, args);
     if (trace_path && e == cudaSuccess) {
