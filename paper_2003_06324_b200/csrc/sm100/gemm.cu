@@ -67,7 +67,18 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         cfg.ab_format == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     CUtensorMap tmA, tmB, tmB2, tmC;
     CUresult r;
-    if (cfg.a_mn_major)
+    if (cfg.a_mn_major && kMcast == 1) {
+        // (64 rows, K, M/64 panels): box {64, 64, 2} = one slab's two SW128 panels
+        EncodeTiledFn encode = encode_tiled_fn();
+        cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(p.K), static_cast<cuuint64_t>(p.M / 64)};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.lda) * 2, 128};
+        cuuint32_t box[3] = {64, 64, 2};
+        cuuint32_t estr[3] = {1, 1, 1};
+        r = encode ? encode(&tmA, dt, 3, const_cast<void*>(p.A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
+                   : CUDA_ERROR_NOT_INITIALIZED;
+    } else if (cfg.a_mn_major)
         r = encode_2d(&tmA, dt, p.A, p.M, p.K, static_cast<uint64_t>(p.lda) * 2, 64, 64);
     else
         r = encode_2d(&tmA, dt, p.A, p.K, p.M, static_cast<uint64_t>(p.lda) * 2, 64, kMcast > 1 ? 64 : S::BM);

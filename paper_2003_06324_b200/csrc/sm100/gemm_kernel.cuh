@@ -256,8 +256,11 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                             uint8_t* sas = sa + sl * S::SLAB_BYTES;
                             const int m0s = m0 + sl * S::BM_MMA;
                             if (args.a_mn_major) {
-                                load(sas, &tmA, m0s, k0, pol_a);
-                                load(sas + 8192, &tmA, m0s + 64, k0, pol_a);
+                                // one 3D box {64, 64, 2}: both 64-row SW128 panels of the slab
+                                // (tmA viewed as 64 rows x K x M/64 panels) -- one TMA op instead
+                                // of two; the SM's TMA unit is a bottleneck of the main loop
+                                if constexpr (kCtaGroup == 1) tma_load_3d(sas, &tmA, &full_bar[s], 0, k0, m0s / 64);
+                                else tma_load_3d_pair(sas, &tmA, &full_bar[s], 0, k0, m0s / 64);
                             } else {
                                 load(sas, &tmA, k0, m0s, pol_a);
                             }
