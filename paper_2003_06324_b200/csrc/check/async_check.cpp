@@ -554,15 +554,19 @@ private:
                     }
                     release_tmem();
                 } else if (whole && a_.c_tma) {
-                    // double-buffered epi staging, one TMA store per chunk
+                    // chunk pairs staged in both epi buffers, one 64-column TMA store per pair
                     for (int c = 0; c < nch_all; ++c) {
                         tmem(E, cta, buf, c * 32, 32, false);
-                        const long off = static_cast<long>(epi_chunk++ & 1) * kChunkBytes;
-                        wait_groups(cta, 1, false);  // bulk_wait_group_read<1> + epilogue_bar
+                        const long off = static_cast<long>(c & 1) * kChunkBytes;
+                        if ((c & 1) == 0) wait_groups(cta, 0, false);  // bulk_wait_group_read<0> + epilogue_bar
                         smem(E, cta, kEpi, off, kChunkBytes, true);
-                        bulk_store(kEpi, off, [&](int bw) { store_c(bw, tile, cchunk(c)); });
-                        commit_group(cta);
+                        if (c & 1) {
+                            bulk_store(kEpi, 0, [&](int bw) { store_c(bw, tile, cchunk(c - 1)); });
+                            bulk_store(kEpi, kChunkBytes, [&](int bw) { store_c(bw, tile, cchunk(c)); });
+                            commit_group(cta);
+                        }
                     }
+                    wait_groups(cta, 0, false);  // the epi buffers are free for the next unit
                     release_tmem();
                 } else if (whole) {
                     for (int c = 0; c < nch_all; ++c) {

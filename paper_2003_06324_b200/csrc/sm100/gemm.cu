@@ -65,7 +65,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
 
     const CUtensorMapDataType dt =
         cfg.ab_format == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-    CUtensorMap tmA, tmB, tmB2, tmC;
+    CUtensorMap tmA, tmB, tmB2, tmC, tmC2;
     CUresult r;
     if (cfg.a_mn_major && kMcast == 1) {
         // (64 rows, K, M/64 panels): box {64, 64, 2} = one slab's two SW128 panels
@@ -105,8 +105,13 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         r = encode_2d(&tmC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p.C, p.M, p.N, static_cast<uint64_t>(p.ldc) * 4,
                       S::BM, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
         if (r != CUDA_SUCCESS) return kTcErrTensorMap;
+        // 64-column box: two adjacent staged chunks in one store
+        r = encode_2d(&tmC2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p.C, p.M, p.N, static_cast<uint64_t>(p.ldc) * 4,
+                      S::BM, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (r != CUDA_SUCCESS) return kTcErrTensorMap;
     } else {
         tmC = tmA;  // unused
+        tmC2 = tmA;
     }
 
     GemmArgs args;
@@ -287,7 +292,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         attrs[lc.numAttrs].val.cooperative = 1;
         ++lc.numAttrs;
     }
-    cudaError_t e = cudaLaunchKernelEx(&lc, kernel, tmA, tmB, tmB2, tmC, args);
+    cudaError_t e = cudaLaunchKernelEx(&lc, kernel, tmA, tmB, tmB2, tmC, tmC2, args);
     if (trace_path && e == cudaSuccess) {
         std::vector<unsigned long long> h(trace_n);
         cudaMemcpyAsync(h.data(), trace_buf, trace_n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);

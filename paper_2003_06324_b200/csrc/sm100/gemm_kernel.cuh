@@ -118,6 +118,7 @@ __device__ __forceinline__ void epilogue_bar() { asm volatile("bar.sync 1, 128;"
 template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves, int kMcast>
 __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                                    const CUtensorMap& tmB2, const CUtensorMap& tmC,
+                                                   const CUtensorMap& tmC2,
                                                    const GemmArgs& args) {
     using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
     static_assert(kSlabs * kNHalves == 1 || (kCtaGroup == 2 && kSplitK == 1 && kSlabs * kNHalves == 2),
@@ -444,8 +445,9 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
                     float* stage0 = reinterpret_cast<float*>(ring);
                     drain_pairs(tbase, nch_all, [&](int c) { return stage0 + c * (32 * S::BM); },
-                                [&](int c) {
-                                    tma_store_2d(&tmC, stage0 + c * (32 * S::BM), m_cta + chunk_row(c), chunk_col(c));
+                                [&](int c) {  // chunks c, c+1 are adjacent in smem and in C: one 64-column box
+                                    if ((c & 1) == 0)
+                                        tma_store_2d(&tmC2, stage0 + c * (32 * S::BM), m_cta + chunk_row(c), chunk_col(c));
                                 });
                     release_tmem();
                 } else if (u.k0 == 0 && u.k1 == kb && args.c_tma) {
@@ -453,24 +455,33 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     // Column j of a chunk is 128 contiguous rows (512 B): thread `row`
                     // writes bank row % 32, conflict-free; one thread stores the chunk.
                     const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
+                    // chunk pairs fill both epi buffers, then ONE 64-column TMA store
+                    // (half the store ops: the SM's TMA unit also feeds the next main loop)
 #pragma unroll 1
                     for (int c = 0; c < nch_all; ++c) {
                         uint32_t r[32];
                         tmem_ld_32x32b_x32(tbase + c * 32, r);
-                        float* stage = epi + (epi_chunk++ & 1) * (32 * S::BM);
-                        if (q == 0 && lane == 0) bulk_wait_group_read<1>();  // the store 2 chunks ago left it
-                        epilogue_bar();
+                        float* stage = epi + (c & 1) * (32 * S::BM);
+                        if ((c & 1) == 0) {
+                            if (q == 0 && lane == 0) bulk_wait_group_read<0>();  // the previous pair's store left epi
+                            epilogue_bar();
+                        }
                         tmem_ld_wait();
 #pragma unroll
                         for (int j = 0; j < 32; ++j) stage[j * S::BM + row] = __uint_as_float(r[j]);
-                        fence_proxy_async();
-                        epilogue_bar();
-                        if (q == 0 && lane == 0) {
-                            tma_store_2d(&tmC, stage, m_cta + chunk_row(c), chunk_col(c));
-                            bulk_commit_group();
+                        if (c & 1) {
+                            fence_proxy_async();
+                            epilogue_bar();
+                            if (q == 0 && lane == 0) {
+                                tma_store_2d(&tmC2, epi, m_cta + chunk_row(c - 1), chunk_col(c - 1));
+                                bulk_commit_group();
+                            }
+                            __syncwarp();
                         }
-                        __syncwarp();
                     }
+                    // leave the epi buffers free for the next unit's path (each starts
+                    // behind an epilogue barrier this thread also reaches)
+                    if (q == 0 && lane == 0) bulk_wait_group_read<0>();
                     release_tmem();
                 } else if (u.k0 == 0 && u.k1 == kb) {
                     // whole K range (a tile or an N-split half): TMEM -> RF -> GL
@@ -786,8 +797,9 @@ template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves, int kMca
 __global__ void __launch_bounds__(256, 1)
     fi_sm100_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
+                  const __grid_constant__ CUtensorMap tmC2,
                   const __grid_constant__ GemmArgs args) {
-    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kMcast>(tmA, tmB, tmB2, tmC, args);
+    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kMcast>(tmA, tmB, tmB2, tmC, tmC2, args);
 }
 
 }  // namespace fireiron::sm100
