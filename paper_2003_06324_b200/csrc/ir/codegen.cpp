@@ -350,8 +350,9 @@ KernelSource generate(const Program& prog) {
           << "__global__ void __launch_bounds__(256, 1) " << prog.entry_name
           << "(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,\n"
           << "    const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,\n"
+          << "    const __grid_constant__ CUtensorMap tmC2,\n"
           << "    const __grid_constant__ GemmArgs args) {\n"
-          << "  fi_sm100_gemm_body<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves, kMcast>(tmA, tmB, tmB2, tmC, args);\n"
+          << "  fi_sm100_gemm_body<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves, kMcast>(tmA, tmB, tmB2, tmC, tmC2, args);\n"
           << "}\n"
           << "}  // namespace fi_generated\n";
         ks.source = o.str();

@@ -24,7 +24,8 @@ inline GemmArgs matmul_8192x8192x8192_args(void* C) {
 }
 __global__ void __launch_bounds__(256, 1) matmul_8192x8192x8192(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
     const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
+    const __grid_constant__ CUtensorMap tmC2,
     const __grid_constant__ GemmArgs args) {
-  fi_sm100_gemm_body<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves, kMcast>(tmA, tmB, tmB2, tmC, args);
+  fi_sm100_gemm_body<kCtaGroup, kMmaN, kSplitK, kSlabs, kNHalves, kMcast>(tmA, tmB, tmB2, tmC, tmC2, args);
 }
 }  // namespace fi_generated
