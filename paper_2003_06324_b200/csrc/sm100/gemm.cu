@@ -285,7 +285,12 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     // each wait on CTAs of their own that cannot be scheduled)
     static const bool coop_env = [] {
         const char* v = std::getenv("FI_TC_COOP");
-        return !(v && v[0] == '0');
+        if (v) return v[0] != '0';
+        // Nsight Compute replays each launch in passes and rejects cooperative
+        // cluster launches (LaunchFailed): under a Nsight tool launch normally
+        // (the kernel is profiled alone, so co-residency is not at risk)
+        return !(std::getenv("NV_TPS_LAUNCH_TOKEN") || std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") ||
+                 std::getenv("CUDA_INJECTION64_PATH"));
     }();
     if (sk && coop_env) {
         attrs[lc.numAttrs].id = cudaLaunchAttributeCooperative;
