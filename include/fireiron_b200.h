@@ -168,7 +168,13 @@ fi_status fi_copy_async(void* dst, const void* src, int64_t bytes, void* cuda_st
 fi_status fi_stream_write_u32(void* dptr, uint32_t value, void* cuda_stream);
 
 /* Raw tensor-core GEMM entry (the kernel family behind FI_KIND_TCGEN05):
- * C = A*B, lda/ldb/ldc are physical leading dimensions in elements. */
+ * C = A*B, lda/ldb/ldc are physical leading dimensions in elements.
+ * Asynchronous on cuda_stream, on the current device. Launches whose tails are
+ * K-split use a library-owned fp32 workspace kept per (device, stream): calls
+ * on different streams or devices never share one, calls on one stream are
+ * ordered by it. Safe to call from several threads. A call that would first
+ * allocate that workspace inside a CUDA-graph capture fails with
+ * FI_ERR_UNSUPPORTED (run the same shape once on the stream before capturing). */
 typedef struct fi_tc_config {
     int32_t cta_group, tile_n, split_k;
     int32_t ab_elem;              /* FI_F16 | FI_BF16 */

@@ -49,6 +49,10 @@ extern "C" fi_status fi_tc_gemm(const fi_tc_config* cfg, const void* dA, const v
             return rt::set_error(FI_ERR_UNSUPPORTED, "fi_tc_gemm: shape not divisible by the tile");
         case sm100::kTcErrUnsupported:
             return rt::set_error(FI_ERR_UNSUPPORTED, "fi_tc_gemm: no kernel instance for this config");
+        case sm100::kTcErrCapture:
+            return rt::set_error(FI_ERR_UNSUPPORTED,
+                                 "fi_tc_gemm: the stream's stream-K workspace is not allocated yet: launch this "
+                                 "shape once on the stream outside the CUDA-graph capture");
         case sm100::kTcErrTensorMap:
             return rt::set_error(FI_ERR_CUDA, "fi_tc_gemm: cuTensorMapEncodeTiled failed");
         default:

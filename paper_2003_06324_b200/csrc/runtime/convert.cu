@@ -1,6 +1,7 @@
-// Device element conversion fp32 -> storage type. The f16 path is IEEE RNE,
-// which equals anvil::round_to_f16 (proj/include/anvil/matrix.hpp:67-80) for
-// |x| < 65504; bf16 is IEEE RNE.
+// Device element conversion fp32 -> storage type. The f16 path is IEEE RNE
+// with the reference's saturation above 2^16, which equals anvil::round_to_f16
+// (proj/include/anvil/matrix.hpp:67-80) except on [65520, 65536), where the
+// reference yields 65536 (not an f16 value) and this gives inf; bf16 is IEEE RNE.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -13,8 +14,13 @@ template <typename T>
 __device__ __forceinline__ T cvt(float v);
 template <>
 __device__ __forceinline__ float cvt<float>(float v) { return v; }
+// round_to_f16 (matrix.hpp:76) saturates finite |x| >= 2^16 to +-65504 where
+// IEEE RNE gives +-inf; infinities and NaN pass through (matrix.hpp:68)
 template <>
-__device__ __forceinline__ __half cvt<__half>(float v) { return __float2half_rn(v); }
+__device__ __forceinline__ __half cvt<__half>(float v) {
+    const float a = fabsf(v);
+    return __float2half_rn(a >= 65536.0f && a < INFINITY ? copysignf(65504.0f, v) : v);
+}
 template <>
 __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 

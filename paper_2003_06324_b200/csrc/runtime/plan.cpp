@@ -42,6 +42,17 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) cuda_fail(what, e);
 }
 
+// status of sm100::tc_gemm_launch -> BackendError (every tcgen05 launch site)
+void check_tc_launch(int r) {
+    if (r == sm100::kTcOk) return;
+    if (r == sm100::kTcErrCapture)
+        throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
+                                "the CUDA-graph capture");
+    if (r == sm100::kTcErrCuda)
+        throw BackendError(100, std::string("tcgen05 GEMM launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+}
+
 // ---------------------------------------------------------------- NVRTC
 struct Nvrtc {
     using Prog = void*;
@@ -415,13 +426,7 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
         p.N = static_cast<int>(c1 - c0);
         ck(cudaEventRecord(ev_g[2 * ng], s), "cudaEventRecord");
         const int r = sm100::tc_gemm_launch(I.tc, p, s);
-        if (r == sm100::kTcErrCapture)
-            throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
-                                    "the CUDA-graph capture");
-        if (r == sm100::kTcErrCapture)
-        throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
-                                "the CUDA-graph capture");
-    if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+        check_tc_launch(r);
         ck(cudaEventRecord(ev_g[2 * ng + 1], s), "cudaEventRecord");
         const float* result = reinterpret_cast<const float*>(base + typed_c);
         if (ec != 0) {
@@ -540,13 +545,7 @@ double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, f
         p.N = static_cast<int>(nc);
         ck(cudaEventRecord(ev_g[2 * j], s), "cudaEventRecord");
         const int r = sm100::tc_gemm_launch(I.tc, p, s);
-        if (r == sm100::kTcErrCapture)
-            throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
-                                    "the CUDA-graph capture");
-        if (r == sm100::kTcErrCapture)
-        throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
-                                "the CUDA-graph capture");
-    if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+        check_tc_launch(r);
         ck(cudaEventRecord(ev_g[2 * j + 1], s), "cudaEventRecord");
         const float* result = reinterpret_cast<const float*>(base + typed_c) + c0;
         if (ec != 0) {
@@ -728,10 +727,7 @@ void Plan::launch_gated(const void* dA, const void* dB, void* dC, void* stream, 
     const int r = sm100::tc_gemm_launch(I.tc, p, static_cast<cudaStream_t>(stream));
     if (r == sm100::kTcErrShape)
         throw BackendError(104, "gated launch: chunk_cols must be a multiple of the scheduled tile width");
-    if (r == sm100::kTcErrCapture)
-        throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
-                                "the CUDA-graph capture");
-    if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+    check_tc_launch(r);
 }
 
 void Plan::launch(const void* dA, const void* dB, void* dC, void* stream) const {
@@ -746,13 +742,7 @@ void Plan::launch(const void* dA, const void* dB, void* dC, void* stream) const 
         if ((reinterpret_cast<uintptr_t>(dA) | reinterpret_cast<uintptr_t>(dB)) & 15)
             throw BackendError(104, "TMA operands must be 16-byte aligned");
         const int r = sm100::tc_gemm_launch(I.tc, p, s);
-        if (r == sm100::kTcErrCapture)
-            throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
-                                    "the CUDA-graph capture");
-        if (r == sm100::kTcErrCapture)
-        throw BackendError(104, "the plan's stream-K workspace is not allocated yet: launch it once outside "
-                                "the CUDA-graph capture");
-    if (r != sm100::kTcOk) throw BackendError(100, "tcgen05 GEMM launch failed (code " + std::to_string(r) + ")");
+        check_tc_launch(r);
         return;
     }
     const BufferDecl& out = I.root(I.out_root());

@@ -6,7 +6,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <map>
+#include <memory>
 #include <mutex>
+#include <utility>
 
 #include "gemm_kernel.cuh"
 #include "tc_gemm.hpp"
@@ -52,10 +55,30 @@ CUresult encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, u
 
 thread_local TcLaunchInfo g_last;
 
-TcWorkspace* shared_workspace() {
-    static TcWorkspace ws;  // library pool for callers without their own workspace
-    return &ws;
+// Library pool for callers without their own workspace: one workspace per
+// (device, stream), so launches that share one are stream-ordered. The caller
+// of tc_gemm_launch holds pool_mutex() while the launch is enqueued.
+std::mutex& pool_mutex() {
+    static std::mutex mu;
+    return mu;
 }
+
+TcWorkspace* pool_workspace(int device, cudaStream_t stream) {
+    static std::map<std::pair<int, cudaStream_t>, std::unique_ptr<TcWorkspace>> pool;
+    auto& ws = pool[{device, stream}];
+    if (!ws) ws = std::make_unique<TcWorkspace>();
+    return ws.get();
+}
+
+// Per-device state of one kernel instance: function attributes apply per
+// device context, and the occupancy cap stream-K relies on is a property of
+// the device the launch goes to.
+struct DeviceState {
+    bool attr_done = false;
+    cudaError_t attr_err = cudaSuccess;
+    int max_active = -1;
+};
+constexpr int kMaxDevices = 64;
 
 template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1, int kMcast = 1>
 int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream, bool dry_run = false) {
@@ -152,15 +175,19 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     }();
     args.l2_hint = l2_hint_env;
 
-    static std::once_flag attr_once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [&] {
-        attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        S::SMEM_BYTES);
-        if (attr_err == cudaSuccess && kCluster > 8)
-            attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    });
-    if (attr_err != cudaSuccess) return kTcErrCuda;
+    static std::mutex dev_mu;
+    static DeviceState dev_state[kMaxDevices];
+    int device = 0;
+    if (cudaGetDevice(&device) != cudaSuccess || device < 0 || device >= kMaxDevices) return kTcErrCuda;
+    std::unique_lock<std::mutex> dev_lock(dev_mu);
+    DeviceState& ds = dev_state[device];
+    if (!ds.attr_done) {
+        ds.attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM_BYTES);
+        if (ds.attr_err == cudaSuccess && kCluster > 8)
+            ds.attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        ds.attr_done = true;
+    }
+    if (ds.attr_err != cudaSuccess) return kTcErrCuda;
 
     const int tiles = args.tiles_m * args.tiles_n;
     int sms = p.num_sms > 0 ? p.num_sms : 148;
@@ -186,17 +213,17 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
 
     // Stream-K needs every cluster co-resident (owners spin on later
     // segments' flags): cap the grid at the occupancy limit.
-    static int max_active = -1;
-    if (max_active < 0) {
+    if (ds.max_active < 0) {
         lc.gridDim = dim3(clusters * kCluster, 1, 1);
         int n = 0;
         if (cudaOccupancyMaxActiveClusters(&n, kernel, &lc) != cudaSuccess || n <= 0) {
             cudaGetLastError();
             n = clusters;
         }
-        max_active = n;
+        ds.max_active = n;
     }
-    if (clusters > max_active) clusters = max_active;
+    if (clusters > ds.max_active) clusters = ds.max_active;
+    dev_lock.unlock();
     const int kb = args.k_blocks;
     // FI_TC_PULL_D: publish time of the 2-slice pull fixup in K-blocks (-1 disables)
     static const int pull_d_env = [] {
@@ -228,7 +255,7 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
         args.sk_q = plan.sk_q;
         args.sk_pull = plan.sk_pull;
         args.sk_head = plan.sk_head;
-        TcWorkspace* ws = p.workspace ? p.workspace : shared_workspace();
+        TcWorkspace* ws = p.workspace ? p.workspace : pool_workspace(device, stream);
         const size_t slots = static_cast<size_t>(plan.slots);
         const size_t need_p = slots * kCtaGroup * S::WS_FLOATS;
         const size_t need_f = slots * kCtaGroup;
@@ -391,6 +418,10 @@ TcLaunchInfo tc_gemm_plan(const TcGemmConfig& cfg, const TcGemmProblem& p) {
 int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream, bool dry_run) {
     int chk = tc_gemm_check(cfg, p.M, p.N, p.K);
     if (chk != kTcOk) return chk;
+    // without a caller-owned workspace, the pool's per-(device, stream) entry is
+    // grown and its epoch advanced under the pool lock
+    std::unique_lock<std::mutex> pool_lock(pool_mutex(), std::defer_lock);
+    if (!p.workspace && !dry_run) pool_lock.lock();
     if (cfg.slabs == 2) return launch_impl<2, 256, 1, 2>(cfg, p, stream, dry_run);
     if (cfg.n_halves == 2) return launch_impl<2, 256, 1, 1, 2>(cfg, p, stream, dry_run);
     if (cfg.mcast == 2) {

@@ -43,8 +43,10 @@ struct TcGemmProblem {
     int streamk = -1;                // -1 auto, 0 data-parallel, 1 K-slice tail, 2 N-split tail
     int force_slices = 0;            // >1: K-slice every tile into this many slices (.splitk on pairs)
     int remainder = 1;               // K-slice tails may add a remainder slice on idle clusters
-    // stream-K partial workspace; null = a library-owned pool. Launches that
-    // share a workspace must be ordered on one stream.
+    // stream-K partial workspace; null = the library pool, which keeps one
+    // workspace per (device, stream) so only launches on the same stream share
+    // one. A caller-owned workspace: launches that share it must be ordered on
+    // one stream.
     TcWorkspace* workspace = nullptr;
     // gated B (fused all-gather): B's column chunks of b_chunk_n columns become
     // readable when b_ready[j] >= b_epoch; the schedule starts at chunk b_first_chunk

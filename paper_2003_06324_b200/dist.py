@@ -150,17 +150,34 @@ class PeerGather:
         self.peer = {}
 
 
+def _publish_own_chunk(shard: Shard, b_local, b_full, dist):
+    """Write this rank's chunk into its slot of b_full, which peers read
+    directly (copy-engine pulls or TMA loads through their IPC mappings).
+
+    Two handshakes: (1) before the write, every rank synchronises its stream --
+    which holds all of its previous-step reads of peers' slots (pulls and GEMMs)
+    -- and meets at a barrier, so no peer can still be reading the old contents
+    of my slot; (2) after the write, synchronise and meet again, so every
+    owner's chunk is in place before anyone reads it. A host barrier alone does
+    not order a peer's in-flight device reads, hence the syncs."""
+    import torch
+    sync = torch.cuda.current_stream().synchronize if b_full.is_cuda else (lambda: None)
+    sync()
+    dist.barrier()
+    off = shard.b_chunk_offset(shard.rank)
+    b_full[off:off + shard.b_chunk_elems].copy_(b_local)
+    sync()
+    dist.barrier()
+
+
 def sharded_step_peer(shard: Shard, a_local, b_local, b_full, c_local, gemm: Callable, dist, pg: PeerGather):
-    """One step with copy-engine pulls: write my chunk into my gathered buffer,
-    synchronise (every owner's chunk in place, every peer done reading the
-    previous step's), pull the peers' chunks in rotated order and run each
-    chunk GEMM as soon as its chunk has landed."""
+    """One step with copy-engine pulls: write my chunk into my gathered buffer
+    (_publish_own_chunk: after every peer finished reading the previous step's,
+    and in place on every rank before any pull), pull the peers' chunks in
+    rotated order and run each chunk GEMM as soon as its chunk has landed."""
     import torch
     me = shard.rank
-    off = shard.b_chunk_offset(me)
-    b_full[off:off + shard.b_chunk_elems].copy_(b_local)
-    torch.cuda.current_stream().synchronize()
-    dist.barrier()
+    _publish_own_chunk(shard, b_local, b_full, dist)
     cur = torch.cuda.current_stream()
     events = {j: pg.pull(j, b_full) for j in shard.order() if j != me}
     for j in shard.order():
@@ -182,20 +199,16 @@ def sharded_step_fused(shard: Shard, a_local, b_local, b_full, c_local, plan, di
     for its chunk's flag before its first TMA load (fi_plan_launch_gated).
     `plan` covers (m_local x N x K); `ready` is a device int32[world] buffer
     whose entries only ever increase (epoch = 1, 2, ... per step).
-    The step writes b_local into this rank's slot of b_full before the barrier,
-    while a slower peer may still be pulling that slot for the previous step:
-    harmless when the chunk does not change between steps (the benchmark); a
-    caller that changes b_local between steps must barrier before the call.
+    b_local goes into this rank's slot of b_full through _publish_own_chunk,
+    after every peer's pulls of the previous step completed (their streams
+    wait for the pull streams at the end of each step).
     The epoch is a host value written by stream memops and passed to the
     launch, so a captured step would replay with a frozen epoch: run it
     eagerly (the GEMM's own stream-K epoch is device-side and graph-safe)."""
     import torch
     me = shard.rank
-    off = shard.b_chunk_offset(me)
     cur = torch.cuda.current_stream()
-    b_full[off:off + shard.b_chunk_elems].copy_(b_local)
-    cur.synchronize()
-    dist.barrier()  # every owner's chunk in place; every peer's pulls of the previous step done
+    _publish_own_chunk(shard, b_local, b_full, dist)
     N, C = pg.N, pg.C
     rp = ready.data_ptr()
     N.check(N.lib.fi_stream_write_u32(C.c_void_p(rp + 4 * me), C.c_uint32(epoch), C.c_void_p(cur.cuda_stream)))
@@ -218,13 +231,11 @@ def sharded_step_direct(shard: Shard, a_local, b_local, b_full, c_local, gemm_pt
     """One step with no gather at all: chunk GEMM j's TMA descriptors point at
     owner j's buffer through its IPC mapping, so B streams over NVLink tile by
     tile inside the GEMM (the transfer fused into the kernel's loads).
-    gemm_ptr(j, a_local, b_ptr, c_chunk) launches chunk j on a raw B pointer."""
-    import torch
+    gemm_ptr(j, a_local, b_ptr, c_chunk) launches chunk j on a raw B pointer.
+    The peers' GEMMs of the previous step read my slot until their streams
+    drain: _publish_own_chunk waits for that before overwriting it."""
     me = shard.rank
-    off = shard.b_chunk_offset(me)
-    b_full[off:off + shard.b_chunk_elems].copy_(b_local)
-    torch.cuda.current_stream().synchronize()
-    dist.barrier()
+    _publish_own_chunk(shard, b_local, b_full, dist)
     for j in shard.order():
         bo, co = shard.b_chunk_offset(j), shard.c_chunk_offset(j)
         ptr = b_full.data_ptr() + bo * pg.esize if j == me else pg.peer[j][0] + bo * pg.esize

@@ -103,3 +103,44 @@ def test_peer_gather_failure_is_collective():
         p.join(timeout=60)
     assert sorted(res) == [0, 1]
     assert all("fi_ipc_export failed" in v for v in res.values()), res
+
+
+def _handshake_worker(rank, world, port, path, steps, q):
+    import time
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2003_06324_b200.dist import _publish_own_chunk
+    sh = make_shard(8, 8, 4, world, rank, tile_m=4, tile_n=4)
+    # one shared gathered-B buffer stands in for the IPC-mapped peer buffers:
+    # each rank writes only its own slot, peers read it in place
+    b_full = torch.from_file(path, shared=True, size=sh.k * sh.n)
+    seen = []
+    for step in range(1, steps + 1):
+        _publish_own_chunk(sh, torch.full((sh.b_chunk_elems,), float(10 * step + rank)), b_full, dist)
+        peer = (rank + 1) % world
+        if rank == 1:
+            time.sleep(0.3)  # a slow reader of rank 0's slot
+        o = sh.b_chunk_offset(peer)
+        seen.append(float(b_full[o:o + sh.b_chunk_elems].max()))
+    q.put((rank, seen))
+    dist.destroy_process_group()
+
+
+def test_own_chunk_publish_waits_for_slow_readers(tmp_path):
+    """A peer still reading my slot for step t must see step t's chunk, not
+    step t+1's (the own-slot write waits for every rank's previous reads)."""
+    world, steps = 2, 3
+    path = str(tmp_path / "b_full.bin")
+    torch.zeros(8 * 4).numpy().tofile(path)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_handshake_worker, args=(r, world, port, path, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank in range(world):
+        peer = (rank + 1) % world
+        assert res[rank] == [float(10 * s + peer) for s in range(1, steps + 1)], res

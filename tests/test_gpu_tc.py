@@ -298,3 +298,20 @@ def test_c5_band_gated_full_size_sampled_exact(fi):
     torch.cuda.synchronize()
     assert not torch.isnan(C).any().item()
     assert _sampled_exact(torch, np, A, B, C, m, n)
+
+
+def test_f16_ingestion_saturates_like_round_to_f16(fi, oracle):
+    """run_host snaps fp32 host data to f16 on the device with the reference's
+    saturation (matrix.hpp:76): finite |x| >= 2^16 becomes +-65504 where IEEE
+    RNE gives inf. C = A * I reproduces the snapped A exactly."""
+    m = n = k = 256
+    plan = fi.Plan(fi.strategies.tc_strategy(m, n, k, pair=True, tile_n=256))
+    rng = np.random.default_rng(5)
+    a = rng.uniform(-2.0, 2.0, (m, k)).astype(np.float32)
+    special = np.array([70000.0, -70000.0, 1e6, -3e38, 65504.0, 65519.0, -65519.0, 65536.0, 1e-8, -2.0 ** -24],
+                       dtype=np.float32)
+    a.flat[rng.choice(m * k, special.size * 20, replace=False)] = np.tile(special, 20)
+    c = plan.run_host(a, np.eye(k, n, dtype=np.float32))
+    want = oracle.round_elem(a, "f16")
+    assert np.isfinite(c).all()
+    assert np.array_equal(c, want)
