@@ -18,6 +18,7 @@ CASES = {
     "move_identity": lambda: (G / "listings/move_identity.fi").read_text(),
     "corpus_seed03": lambda: (G / "corpus/seed03.fi").read_text(),
     "reuse_buffer": lambda: (ROOT / "tests/fixtures/reuse_buffer.fi").read_text(),
+    "paper_wmma": lambda: fi.strategies.wmma_decomp(256, 256, 256),
     "c2_tcgen05": fi.strategies.c2_strategy,
     "c3_splitk": fi.strategies.c3_strategy,
     "pair512_slabs": lambda: fi.strategies.tc_strategy(8192, 8192, 8192, tile_m=512),

@@ -58,7 +58,10 @@ struct Emitter {
         }
         return emit_c(simplify(iadd(imul(row, iconst(rs)), imul(col, iconst(cs)))));
     }
-    std::string ref_text(const ElemRef& r) const { return storage_name(r.buf) + "[" + offset_text(r) + "]"; }
+    // every shared buffer, aliases included, is a pointer of its own element
+    // type into its storage root (sim.hpp:314-320 indexes an alias by element
+    // in its own geometry; its stores round by its own type, sim.hpp:336-339)
+    std::string ref_text(const ElemRef& r) const { return buf(r.buf).name + "[" + offset_text(r) + "]"; }
     std::string load_text(const ElemRef& r) const { return "fi_ld(" + ref_text(r) + ")"; }
     std::string store_text(const ElemRef& r, const std::string& value) const {
         return ref_text(r) + " = fi_st<" + std::string(storage_type(buf(r.buf).elem)) + ">(" + value + ");";
@@ -166,7 +169,7 @@ struct Emitter {
                 const BufferDecl& b = buf(r->buf);
                 const bool local = b.distributed_rf();
                 if (field.empty()) value = ref_text(*r);
-                else if (field == "base") value = storage_name(r->buf);
+                else if (field == "base") value = b.name;
                 else if (field == "off") value = offset_text(*r);
                 else if (field == "rs") value = std::to_string(local ? b.local_row_stride() : b.row_stride());
                 else if (field == "cs") value = std::to_string(local ? b.local_col_stride() : b.col_stride());
@@ -207,12 +210,10 @@ struct Emitter {
             const std::string t = storage_type(b.elem);
             switch (b.mem.kind) {
                 case MemKind::SH:
-                    if (b.alias_of >= 0) {
+                    if (b.alias_of >= 0)
                         line("// " + b.name + " aliases " + storage_name(b.id) + " (reuseBuffer)");
-                        break;
-                    }
                     line(t + "* const " + b.name + " = reinterpret_cast<" + t + "*>(fi_smem + " +
-                         std::to_string(sh_offset[b.id]) + ");");
+                         std::to_string(sh_offset[prog.plan.storage_root(b.id)]) + ");");
                     break;
                 case MemKind::RF:
                     line(t + " " + b.name + "[" + std::to_string(b.distributed_rf() ? b.local_extent() : b.extent()) +
@@ -270,7 +271,7 @@ struct Emitter {
         line("template <> __device__ __forceinline__ float fi_st<float>(float v) { return v; }");
         line("// round_to_f16 saturates at +-65504 above 2^16 (anvil matrix.hpp:76)");
         line("template <> __device__ __forceinline__ __half fi_st<__half>(float v) {");
-        line("  return __float2half_rn(fabsf(v) >= 65536.0f && fabsf(v) < INFINITY ? copysignf(65504.0f, v) : v);");
+        line("  return __float2half_rn(fabsf(v) >= 65536.0f && fabsf(v) <= 3.40282347e38f ? copysignf(65504.0f, v) : v);");
         line("}");
         line("template <> __device__ __forceinline__ __nv_bfloat16 fi_st<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }");
         line("// the FMA leaf: product and sum each rounded to fp32 (sim.hpp:370-376)");

@@ -19,7 +19,7 @@ __device__ __forceinline__ float cvt<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ __half cvt<__half>(float v) {
     const float a = fabsf(v);
-    return __float2half_rn(a >= 65536.0f && a < INFINITY ? copysignf(65504.0f, v) : v);
+    return __float2half_rn(a >= 65536.0f && a <= 3.40282347e38f ? copysignf(65504.0f, v) : v);
 }
 template <>
 __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }

@@ -10,7 +10,7 @@ template <typename T> __device__ __forceinline__ T fi_st(float v);
 template <> __device__ __forceinline__ float fi_st<float>(float v) { return v; }
 // round_to_f16 saturates at +-65504 above 2^16 (anvil matrix.hpp:76)
 template <> __device__ __forceinline__ __half fi_st<__half>(float v) {
-  return __float2half_rn(fabsf(v) >= 65536.0f && fabsf(v) < INFINITY ? copysignf(65504.0f, v) : v);
+  return __float2half_rn(fabsf(v) >= 65536.0f && fabsf(v) <= 3.40282347e38f ? copysignf(65504.0f, v) : v);
 }
 template <> __device__ __forceinline__ __nv_bfloat16 fi_st<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 // the FMA leaf: product and sum each rounded to fp32 (sim.hpp:370-376)

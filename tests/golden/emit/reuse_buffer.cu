@@ -10,7 +10,7 @@ template <typename T> __device__ __forceinline__ T fi_st(float v);
 template <> __device__ __forceinline__ float fi_st<float>(float v) { return v; }
 // round_to_f16 saturates at +-65504 above 2^16 (anvil matrix.hpp:76)
 template <> __device__ __forceinline__ __half fi_st<__half>(float v) {
-  return __float2half_rn(fabsf(v) >= 65536.0f && fabsf(v) < INFINITY ? copysignf(65504.0f, v) : v);
+  return __float2half_rn(fabsf(v) >= 65536.0f && fabsf(v) <= 3.40282347e38f ? copysignf(65504.0f, v) : v);
 }
 template <> __device__ __forceinline__ __nv_bfloat16 fi_st<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 // the FMA leaf: product and sum each rounded to fp32 (sim.hpp:370-376)
@@ -26,6 +26,7 @@ extern "C" __global__ void __launch_bounds__(128) matmul_64x64x32(const float* _
   float A_rf_13[4];
   float B_rf_15[8];
   // SRC_sh_18 aliases A_sh_6 (reuseBuffer)
+  float* const SRC_sh_18 = reinterpret_cast<float*>(fi_smem + 0);
 
   for (int row4 = 0; row4 < 4; ++row4) {
     for (int col4 = 0; col4 < 8; ++col4) {
@@ -60,13 +61,13 @@ extern "C" __global__ void __launch_bounds__(128) matmul_64x64x32(const float* _
   }
   for (int row21 = 0; row21 < 4; ++row21) {
     for (int col21 = 0; col21 < 8; ++col21) {
-      A_sh_6[((((((threadIdx.x / 32) % 2) * 32) + (((threadIdx.x % 32) % 8) * 4)) + row21) + ((((((threadIdx.x / 32) / 2) * 32) + (((threadIdx.x % 32) / 8) * 8)) + col21) * 64))] = fi_st<float>(fi_ld(C_rf_1[(row21 + (col21 * 4))]));
+      SRC_sh_18[((((((threadIdx.x / 32) % 2) * 32) + (((threadIdx.x % 32) % 8) * 4)) + row21) + ((((((threadIdx.x / 32) / 2) * 32) + (((threadIdx.x % 32) / 8) * 8)) + col21) * 64))] = fi_st<float>(fi_ld(C_rf_1[(row21 + (col21 * 4))]));
     }
   }
   __syncthreads();
   for (int row24 = 0; row24 < 4; ++row24) {
     for (int col24 = 0; col24 < 8; ++col24) {
-      C[(((((blockIdx.x * 64) + (((threadIdx.x / 32) % 2) * 32)) + (((threadIdx.x % 32) % 8) * 4)) + row24) + (((((blockIdx.y * 64) + (((threadIdx.x / 32) / 2) * 32)) + (((threadIdx.x % 32) / 8) * 8)) + col24) * 64))] = fi_st<float>(fi_ld(A_sh_6[((((((threadIdx.x / 32) % 2) * 32) + (((threadIdx.x % 32) % 8) * 4)) + row24) + ((((((threadIdx.x / 32) / 2) * 32) + (((threadIdx.x % 32) / 8) * 8)) + col24) * 64))]));
+      C[(((((blockIdx.x * 64) + (((threadIdx.x / 32) % 2) * 32)) + (((threadIdx.x % 32) % 8) * 4)) + row24) + (((((blockIdx.y * 64) + (((threadIdx.x / 32) / 2) * 32)) + (((threadIdx.x % 32) / 8) * 8)) + col24) * 64))] = fi_st<float>(fi_ld(SRC_sh_18[((((((threadIdx.x / 32) % 2) * 32) + (((threadIdx.x % 32) % 8) * 4)) + row24) + ((((((threadIdx.x / 32) / 2) * 32) + (((threadIdx.x % 32) / 8) * 8)) + col24) * 64))]));
     }
   }
 }

@@ -39,6 +39,15 @@ def test_wmma_listing_compiles_for_sm100a(fi, tmp_path):
     assert "HMMA" in sass
 
 
+def test_paper_wmma_strategy_compiles(fi, tmp_path):
+    """the f32 epilog staging buffer reuses A's f16 shared
+    storage (reuseBuffer) and is emitted as its own f32 view of it."""
+    src = fi.generate(fi.strategies.wmma_decomp(1024, 1024, 1024))
+    assert "float* const SRC_sh" in src
+    sass = compile_sass(src, tmp_path)
+    assert "HMMA" in sass
+
+
 @pytest.mark.parametrize("key", ["corpus/seed03", "corpus/seed17", "corpus/seed42", "listings/move_identity"])
 def test_corpus_kernels_compile(fi, key, tmp_path):
     compile_sass(fi.generate(golden_script(key)), tmp_path)
@@ -61,3 +70,44 @@ def test_native_library_contains_tcgen05_family(fi):
     sass = subprocess.run(["cuobjdump", "-sass", fi.LIB_PATH], capture_output=True, text=True).stdout
     for mnemonic in ("UTCHMMA.2CTA", "UTCHMMA", "UTMALDG.2D", "LDTM", "UTCBAR"):
         assert mnemonic in sass, mnemonic
+
+
+def _nvrtc_compile(src: str):
+    """Compile as the runtime does (runtime/plan.cpp compile_cubin: NVRTC,
+    sm_100a, --fmad=false); returns (ok, log). NVRTC needs no GPU."""
+    import ctypes as C
+    lib = None
+    for name in ("libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12"):
+        try:
+            lib = C.CDLL(name)
+            break
+        except OSError:
+            pass
+    if lib is None:
+        pytest.skip("libnvrtc absent")
+    prog = C.c_void_p()
+    assert lib.nvrtcCreateProgram(C.byref(prog), src.encode(), b"k.cu", 0, None, None) == 0
+    opts = [b"--gpu-architecture=sm_100a", b"--fmad=false", b"-std=c++17", b"-default-device", b"-lineinfo",
+            b"--include-path=/usr/local/cuda/include"]
+    rc = lib.nvrtcCompileProgram(prog, len(opts), (C.c_char_p * len(opts))(*opts))
+    n = C.c_size_t()
+    lib.nvrtcGetProgramLogSize(prog, C.byref(n))
+    log = C.create_string_buffer(n.value)
+    lib.nvrtcGetProgramLog(prog, log)
+    lib.nvrtcDestroyProgram(C.byref(prog))
+    return rc == 0, log.value.decode(errors="replace")
+
+
+@pytest.mark.parametrize("key", ["listings/listing2", "listings/wmma_simple", "listings/move_identity",
+                                 "corpus/seed03", "paper_wmma", "listing2_f16"])
+def test_generic_sources_compile_with_nvrtc(fi, key):
+    if key == "paper_wmma":
+        script = fi.strategies.wmma_decomp(256, 256, 256)
+    elif key == "listing2_f16":
+        lines = golden_script("listings/listing2").splitlines()
+        lines[0] += " elems f16 f16 f16"
+        script = "\n".join(lines) + "\n"
+    else:
+        script = golden_script(key)
+    ok, log = _nvrtc_compile(fi.generate(script))
+    assert ok, log

@@ -127,3 +127,33 @@ def test_micro_kernel_strategy_runs_verbatim(fi, oracle):
     b = oracle.fill(64, 256, 8, False)
     got = plan.run_host(a, b)
     assert np.array_equal(got.view(np.uint32), oracle.seqk_f32(a, b).view(np.uint32))
+
+
+@needs_ref
+@pytest.mark.parametrize("integers", [True, False], ids=["int", "uniform"])
+def test_paper_wmma_strategy_matches_reference(fi, oracle, integers):
+    """The paper's staged WMMA strategy: its epilog stages
+    the f32 accumulators through an SH buffer that reuses A's f16 storage
+    (reuseBuffer); the alias is its own f32 view of that storage, as in the
+    simulator (sim.hpp:314-339). Integer inputs: exact; uniform inputs: within
+    the reference's WMMA bound 2^-8 (test_acceptance.cpp:132-154)."""
+    m = n = k = 256
+    s = fi.strategies.wmma_decomp(m, n, k)
+    a = oracle.fill(m, k, 41, integers)
+    b = oracle.fill(k, n, 42, integers)
+    want, races = oracle.ref_run(s, a, b)
+    assert races == 0
+    got = fi.Plan(s).run_host(a, b)
+    if integers:
+        assert np.array_equal(got, want)
+    else:
+        assert oracle.max_abs_error(got, want) <= 2.0 ** -8
+
+
+def test_paper_wmma_strategy_1024_vs_f64(fi, oracle):
+    m = n = k = 1024
+    plan = fi.Plan(fi.strategies.wmma_decomp(m, n, k))
+    assert plan.kind == "generic"
+    a = oracle.fill(m, k, 3, True)
+    b = oracle.fill(k, n, 4, True)
+    assert np.array_equal(plan.run_host(a, b), oracle.gemm_f64(a, b))
