@@ -37,6 +37,7 @@ sys.path.insert(0, ROOT)
 METRIC = "GEMM TFLOP/s (fp16 in/fp32 acc) and % of B200 tensor peak at 1/2/4/8 GPUs"
 UNIT = "TFLOP/s"
 L2_FLUSH_BYTES = 512 << 20
+DATA = "synthetic (uniform [-1,1) matrices; no dataset)"
 
 
 def load_peaks():
@@ -60,6 +61,18 @@ def workload_of(args, world):
     if w == "c5":
         return dict(name="c5_16384^3_bf16_sharded_MN_allgatherB", m=16384, n=16384, k=16384, ab="bf16")
     raise SystemExit(f"unknown workload {w}")
+
+
+def problem_config(wl, world):
+    """The `config` both arms print (identical, so the driver can pair them):
+    the problem only. Each arm's implementation details go under `impl_config`."""
+    cfg = {"workload": wl["name"], "m": wl["m"], "n": wl["n"], "k": wl["k"],
+           "ab_type": wl["ab"], "c_type": "f32", "layout": "col-major A, B, C (Fireiron default)",
+           "inputs": "synthetic uniform [-1,1), snapped to the A/B type",
+           "l2": "GPU arm: flushed (512 MiB write) before every timed step"}
+    if world > 1:
+        cfg["parallelism"] = f"mn-shard{world}"
+    return cfg
 
 
 def strategy_for(fi, wl, m, n, k):
@@ -190,11 +203,15 @@ def reference_arm(args, fi, rank, world):
     flops = 2.0 * wl["m"] * wl["n"] * wl["k"]
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": secs / len(vals) * 1e3, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32 (CPU simulator)",
-            "data": "synthetic (splitmix64 uniform fills)",
-            "config": {"workload": wl["name"], "m": wl["m"], "n": wl["n"], "k": wl["k"],
-                       "strategy": "paper WMMA decomposition (GL->SH->FR, WMMA leaves) on the anvil CPU model",
-                       "extrapolated_full_problem_s": flops / (v * 1e12)},
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": wl["ab"] + " in / f32 acc",
+            "data": DATA,
+            "config": problem_config(wl, world),
+            "impl_config": {"engine": "reference CPU simulator (oracle/_ref: anvil::detail::Machine, unmodified "
+                                      "headers built in place)",
+                            "strategy": "paper WMMA decomposition (GL->SH->FR, WMMA leaves; f16 inputs, fp32 "
+                                        "accumulate) on the anvil CPU model",
+                            "inputs": "splitmix64 uniform fills (the reference's own generator)",
+                            "extrapolated_full_problem_s": flops / (v * 1e12)},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": vals[-1]["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -284,12 +301,14 @@ def ours_single(args, fi, torch):
     info = plan.info
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_mean, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": wl["ab"] + " in / f32 acc", "data": "synthetic (uniform [-1,1) on device)",
-            "config": {"workload": wl["name"], "m": m, "n": n, "k": k, "tile": f"{info.tile_m}x{info.tile_n}",
-                       "cta_group": info.cta_group, "split_k": info.split_k, "stages": info.stages,
-                       "ctas": info.launch_ctas, "l2": "flushed (512 MiB write) before every timed step",
-                       "percent_of_peak": 100.0 * value / peaks["tflops"],
-                       "ms_min": min(ms), "ms_median": statistics.median(ms), "wall_s": wall},
+            "dtype": wl["ab"] + " in / f32 acc", "data": DATA,
+            "config": problem_config(wl, 1),
+            "impl_config": {"engine": "tcgen05 persistent GEMM (TMA -> SW128 smem ring -> tcgen05.mma -> TMEM)",
+                            "tile": f"{info.tile_m}x{info.tile_n}",
+                            "cta_group": info.cta_group, "split_k": info.split_k, "stages": info.stages,
+                            "ctas": info.launch_ctas, "inputs": "torch uniform [-1,1) generated on the device",
+                            "percent_of_peak": 100.0 * value / peaks["tflops"],
+                            "ms_min": min(ms), "ms_median": statistics.median(ms), "wall_s": wall},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": flops / e2e_s / 1e12, "unit": UNIT,
@@ -415,9 +434,9 @@ def ours_multi(args, fi, torch, rank, world):
         peaks = load_peaks()
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": wl["ab"] + " in / f32 acc", "data": "synthetic (uniform on device)",
-                "config": {"workload": wl["name"], "m": m, "n": n, "k": k, "parallelism": f"mn-shard{world}",
-                           "shard": f"{shard.m_local}x{n} rows of C per GPU, B chunks of {shard.n_chunk} columns",
+                "vs_baseline": None, "dtype": wl["ab"] + " in / f32 acc", "data": DATA,
+                "config": problem_config(wl, world),
+                "impl_config": {"shard": f"{shard.m_local}x{n} rows of C per GPU, B chunks of {shard.n_chunk} columns",
                            "comm": {"fused": "copy-engine pulls of B chunks from IPC-mapped peer buffers in "
                                              "rotated order, each releasing a ready flag to ONE gated persistent "
                                              "GEMM over the whole C band (tiles wait per chunk)",
@@ -425,8 +444,7 @@ def ours_multi(args, fi, torch, rank, world):
                                             "overlapped with chunk GEMMs",
                                     "direct": "chunk GEMMs read B over NVLink from the owners' IPC-mapped buffers",
                                     }.get(transport, "NCCL per-owner broadcasts of B chunks, overlapped with chunk GEMMs"),
-                           "percent_of_peak": 100.0 * value / (world * peaks["tflops"]),
-                           "l2": "flushed before every timed step"},
+                           "percent_of_peak": 100.0 * value / (world * peaks["tflops"])},
                 "roofline": {"bound": "tensor", "achieved": value / world, "peak": peaks["tflops"], "unit": UNIT,
                              "frac": value / world / peaks["tflops"], "traffic": None,
                              "peak_source": f"{peaks['src']} bf16_tflops per GPU"},
