@@ -152,6 +152,13 @@ int64_t fi_script_plan(const char* script_utf8, int64_t m, int64_t n, int64_t k,
  * matrix.hpp:67-80, for |x| < 65504). */
 fi_status fi_convert_f32(const float* src, void* dst, int64_t count, int elem, void* cuda_stream);
 
+/* Host-side conversion fp32 -> {f16 (elem 1), bf16 (elem 2)} on the calling
+ * thread, bit-identical to fi_convert_f32 (the f16 path also saturates finite
+ * |x| >= 2^16 to +-65504; NaN becomes 0x7FFF). fi_plan_run_host uses it, on a
+ * pool of host threads, to snap input panels before they cross PCIe
+ * (FI_HOST_SNAP=0 disables). FI_ERR_UNSUPPORTED when the CPU lacks AVX2/F16C. */
+fi_status fi_host_snap_f32(const float* src, void* dst, int64_t count, int elem);
+
 /* Multi-GPU driver (one process per GPU): CUDA IPC export of a device buffer
  * (handle of its allocation + the pointer's offset into it), import of a
  * peer's buffer, and a stream-ordered copy (copy engines; over NVLink/NVSwitch

@@ -80,6 +80,7 @@ def _load() -> C.CDLL:
         "fi_last_error": ([], C.c_char_p),
         "fi_tc_gemm": ([C.POINTER(TcConfig), vp, vp, vp, i64, i64, i64, i64, i64, i64, vp, vp], C.c_int),
         "fi_convert_f32": ([vp, vp, i64, C.c_int, vp], C.c_int),
+        "fi_host_snap_f32": ([vp, vp, i64, C.c_int], C.c_int),
         "fi_ipc_export": ([vp, vp, C.POINTER(i64)], C.c_int),
         "fi_ipc_open": ([vp, i64, C.POINTER(vp)], C.c_int),
         "fi_ipc_close": ([vp, i64], C.c_int),

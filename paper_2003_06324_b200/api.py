@@ -108,6 +108,16 @@ def check_async(script: str, m: int = 0, n: int = 0, k: int = 0, *, num_sms: int
     return AsyncReport(_text(N.lib.fi_script_check_async, _enc(script), m, n, k, C.byref(o)))
 
 
+def host_snap(x: np.ndarray, elem: str = "f16") -> np.ndarray:
+    """fp32 -> f16/bf16 bit patterns (uint16) on the host, as fi_plan_run_host
+    snaps input panels before they cross PCIe (fi_host_snap_f32)."""
+    src = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty(src.shape, dtype=np.uint16)
+    code = {"f16": 1, "bf16": 2}[elem]
+    N.check(N.lib.fi_host_snap_f32(src.ctypes.data, out.ctypes.data, src.size, code))
+    return out
+
+
 def _np_elem(code: int):
     return {N.FI_F32: np.float32, N.FI_F16: np.float16}.get(code)
 

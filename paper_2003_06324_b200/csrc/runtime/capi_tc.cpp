@@ -5,6 +5,7 @@
 
 #include "../../../include/fireiron_b200.h"
 #include "../sm100/tc_gemm.hpp"
+#include "host_snap.hpp"
 #include "status.hpp"
 
 namespace fireiron::rt {
@@ -67,5 +68,14 @@ extern "C" fi_status fi_convert_f32(const float* src, void* dst, int64_t count, 
     cudaError_t e = rt::convert_f32(src, dst, count, elem, static_cast<cudaStream_t>(cuda_stream));
     if (e != cudaSuccess)
         return rt::set_error(FI_ERR_CUDA, std::string("fi_convert_f32: ") + cudaGetErrorString(e));
+    return FI_OK;
+}
+
+extern "C" fi_status fi_host_snap_f32(const float* src, void* dst, int64_t count, int elem) {
+    if ((!src || !dst) && count > 0) return rt::set_error(FI_ERR_ARGUMENT, "fi_host_snap_f32: null argument");
+    if (elem != 1 && elem != 2) return rt::set_error(FI_ERR_ARGUMENT, "fi_host_snap_f32: elem must be 1 (f16) or 2 (bf16)");
+    if (!rt::host_snap_supported())
+        return rt::set_error(FI_ERR_UNSUPPORTED, "fi_host_snap_f32: the host CPU lacks AVX2/F16C");
+    if (count > 0) rt::snap_f32(src, static_cast<uint16_t*>(dst), count, elem);
     return FI_OK;
 }

@@ -11,13 +11,17 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <fstream>
+#include <algorithm>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <sstream>
 
 #include "../sm100/tc_gemm.hpp"
+#include "host_snap.hpp"
 #include "fireiron/backend.hpp"
 
 namespace fireiron {
@@ -269,6 +273,9 @@ struct Plan::Impl {
     // pipelined run_host: copy-engine streams (H2D, D2H) and per-chunk events
     mutable cudaStream_t up_stream = nullptr, down_stream = nullptr;
     mutable std::vector<cudaEvent_t> pev;
+    // pinned host staging of host-snapped inputs (typed layout of each root)
+    mutable void* host_stage = nullptr;
+    mutable size_t host_stage_bytes = 0;
 
     ~Impl() {
         if (module) {
@@ -283,6 +290,7 @@ struct Plan::Impl {
         if (up_stream) cudaStreamDestroy(up_stream);
         if (down_stream) cudaStreamDestroy(down_stream);
         for (cudaEvent_t e : pev) cudaEventDestroy(e);
+        if (host_stage) cudaFreeHost(host_stage);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
     }
@@ -369,16 +377,6 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
         ck(cudaStreamCreateWithFlags(&I.up_stream, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&I.down_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     }
-    const int np = P + Q;
-    // events: [start][upload per panel][gemm begin, end per panel][C ready per panel][down done]
-    const size_t need = 1 + np + 2 * np + np + 1;
-    while (I.pev.size() < need) {
-        cudaEvent_t e;
-        ck(cudaEventCreate(&e), "cudaEventCreate");
-        I.pev.push_back(e);
-    }
-    cudaEvent_t* ev = I.pev.data();
-    cudaEvent_t ev_start = ev[0], *ev_up = ev + 1, *ev_g = ev_up + np, *ev_c = ev_g + 2 * np, ev_down = ev_c[np];
     const BufferDecl& ra = I.root(0);
     const BufferDecl& rb = I.root(1);
     const BufferDecl& rc = I.root(2);
@@ -392,20 +390,142 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
     auto c_region = [&](long r0, long r1, long c0, long c1) {
         return c_row ? Region{r0 * ldc + c0, c1 - c0, r1 - r0, ldc} : Region{r0 + c0 * ldc, r1 - r0, c1 - c0, ldc};
     };
-    auto copy2d = [&](void* dst, const void* src, const Region& r, cudaMemcpyKind kind, cudaStream_t st) {
+    auto copy2d = [&](void* dst, const void* src, const Region& r, cudaMemcpyKind kind, cudaStream_t st,
+                      size_t w = 4) {
         if (r.width == r.pitch)  // contiguous lines: one linear copy
-            ck(cudaMemcpyAsync(dst, src, static_cast<size_t>(r.width * r.height) * 4, kind, st), "cudaMemcpyAsync");
+            ck(cudaMemcpyAsync(dst, src, static_cast<size_t>(r.width * r.height) * w, kind, st), "cudaMemcpyAsync");
         else
-            ck(cudaMemcpy2DAsync(dst, r.pitch * 4, src, r.pitch * 4, r.width * 4, r.height, kind, st),
+            ck(cudaMemcpy2DAsync(dst, r.pitch * w, src, r.pitch * w, r.width * w, r.height, kind, st),
                "cudaMemcpy2DAsync");
     };
+    // the panel order: A row panels and B column panels alternately, balanced by bytes
+    const double a_piece = 4.0 * mc * K, b_piece = 4.0 * K * nc;
+    std::vector<char> order;
+    for (int ia = 0, ib = 0; ia < P || ib < Q;) {
+        const bool take_a = ib == Q || (ia < P && ia * a_piece <= ib * b_piece);
+        order.push_back(take_a ? 'A' : 'B');
+        (take_a ? ia : ib)++;
+    }
+    const int np = P + Q;
+    // Each panel crosses PCIe as pieces of whole lines (~FI_HOST_PIECE_MB of
+    // fp32, default 8). Host snapping (runtime/host_snap.hpp): a fraction
+    // FI_HOST_SNAP_RATIO (default 0.8) of the pieces of f16/bf16 roots, spread
+    // evenly over the upload order, is converted by host cores into pinned
+    // staging while the copy engine moves the others as fp32 (snapped on the
+    // device), and then crosses in 2-byte elements. The ratio balances the two
+    // engines measured on the B200 box: the copy engine moves ~54 GB/s, the host
+    // converts ~60 GB/s of fp32 while the copy engine also reads host memory
+    // (profiles/round2/host_snap_probe.txt, host_snap_e2e_ab.log). The first FI_HOST_SNAP_SKIP pieces
+    // (default 1) are snapped on the device so the copy engine starts at once.
+    struct Piece {
+        int panel;
+        bool is_a;
+        Region r;
+        std::unique_ptr<rt::SnapJob> job;
+    };
+    std::vector<Piece> pieces;
+    std::vector<int> panel_end(static_cast<size_t>(np));  // one past each panel's last piece
+    {
+        double piece_bytes = 8.0 * (1 << 20);
+        if (const char* v = std::getenv("FI_HOST_PIECE_MB")) piece_bytes = std::atof(v) * (1 << 20);
+        for (int i = 0, ia = 0, ib = 0; i < np; ++i) {
+            const bool is_a = order[static_cast<size_t>(i)] == 'A';
+            const Region r = is_a ? a_region(ia * mc, (ia + 1) * mc) : b_region(ib * nc, (ib + 1) * nc);
+            (is_a ? ia : ib)++;
+            long nsub = std::lround(4.0 * r.width * r.height / piece_bytes);
+            nsub = std::max(1L, std::min(nsub, r.height));
+            for (long q = 0; q < nsub; ++q) {
+                const long l0 = r.height * q / nsub, l1 = r.height * (q + 1) / nsub;
+                pieces.push_back(Piece{i, is_a, Region{r.off + l0 * r.pitch, r.width, l1 - l0, r.pitch}, nullptr});
+            }
+            panel_end[static_cast<size_t>(i)] = static_cast<int>(pieces.size());
+        }
+    }
+    const int npc = static_cast<int>(pieces.size());
+    // events: [start][upload per piece][gemm begin, end per panel][C ready per panel][down done]
+    const size_t need = 1 + npc + 2 * np + np + 1;
+    while (I.pev.size() < need) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        I.pev.push_back(e);
+    }
+    cudaEvent_t* ev = I.pev.data();
+    cudaEvent_t ev_start = ev[0], *ev_up = ev + 1, *ev_g = ev_up + npc, *ev_c = ev_g + 2 * np, ev_down = ev_c[np];
+    rt::HostSnapPool* pool = (ea != 0 || eb != 0) ? rt::HostSnapPool::get() : nullptr;
+    if (pool) {
+        size_t hoff[2] = {0, 0}, hbytes = 0;
+        for (int w = 0; w < 2; ++w) {
+            hoff[w] = hbytes;
+            hbytes += (static_cast<size_t>(I.root(w).extent()) * 2 + 255) & ~size_t(255);
+        }
+        if (I.host_stage_bytes < hbytes) {
+            if (I.host_stage) cudaFreeHost(I.host_stage);
+            I.host_stage = nullptr;
+            I.host_stage_bytes = 0;
+            ck(cudaHostAlloc(&I.host_stage, hbytes, cudaHostAllocPortable), "cudaHostAlloc");
+            I.host_stage_bytes = hbytes;
+        }
+        int skip = 1;
+        if (const char* v = std::getenv("FI_HOST_SNAP_SKIP")) skip = std::atoi(v);
+        double ratio = 0.8;
+        if (const char* v = std::getenv("FI_HOST_SNAP_RATIO")) ratio = std::atof(v);
+        // fewer host threads convert proportionally less (16 measured)
+        ratio = std::min(ratio, ratio * (pool->workers() + 1) / 16.0);
+        for (int j = 0, h = 0; j < npc; ++j) {
+            Piece& pc = pieces[static_cast<size_t>(j)];
+            const int elem = pc.is_a ? ea : eb;
+            if (elem == 0 || j < skip) continue;
+            // piece j - skip is host-snapped when the running share crosses an integer
+            const int want = static_cast<int>(std::floor((j - skip + 1) * ratio + 1e-9));
+            if (want <= h) continue;
+            h = want;
+            auto job = std::make_unique<rt::SnapJob>();
+            job->src = (pc.is_a ? A : B) + pc.r.off;
+            job->dst = reinterpret_cast<uint16_t*>(static_cast<char*>(I.host_stage) + hoff[pc.is_a ? 0 : 1]) + pc.r.off;
+            job->width = pc.r.width;
+            job->height = pc.r.height;
+            job->spitch = job->dpitch = pc.r.pitch;
+            job->elem = elem;
+            if (pc.r.width == pc.r.pitch) {  // contiguous: one long line
+                job->width = pc.r.width * pc.r.height;
+                job->height = 1;
+            }
+            pc.job = std::move(job);
+        }
+        for (auto& pc : pieces)  // FIFO: converted in upload order
+            if (pc.job) pool->submit(pc.job.get());
+    }
+    // every submitted job is waited for, also when an upload below throws: the
+    // pool's workers must not touch a job (or the caller's A/B) after we return
+    struct JobGuard {
+        rt::HostSnapPool* pool;
+        std::vector<Piece>& pieces;
+        ~JobGuard() {
+            if (pool)
+                for (auto& pc : pieces)
+                    if (pc.job) pool->wait(pc.job.get());
+        }
+    } job_guard{pool, pieces};
     ck(cudaEventRecord(ev_start, s), "cudaEventRecord");  // scratch reuse: after earlier work on s
     ck(cudaStreamWaitEvent(I.up_stream, ev_start, 0), "cudaStreamWaitEvent");
     ck(cudaStreamWaitEvent(I.down_stream, ev_start, 0), "cudaStreamWaitEvent");
-    // one panel: H2D into the fp32 staging (or straight into an fp32 root), then
-    // snapped to the root's element grid on s (sim.hpp:507-510)
-    auto upload = [&](int which, const float* host, const Region& r, int elem, size_t w, cudaEvent_t done) {
+    // one piece: H2D into the fp32 staging (or straight into an fp32 root), then
+    // snapped to the root's element grid on s (sim.hpp:507-510); or, when host
+    // snapped, H2D of the snapped piece straight into the typed root
+    auto upload = [&](const Piece& pc, cudaEvent_t done) {
+        const int which = pc.is_a ? 0 : 1, elem = pc.is_a ? ea : eb;
+        const size_t w = pc.is_a ? wa : wb;
+        const Region& r = pc.r;
         char* typed = base + typed_in[which];
+        if (pc.job) {
+            pool->wait(pc.job.get());
+            copy2d(typed + static_cast<size_t>(r.off) * w, reinterpret_cast<const char*>(pc.job->dst), r,
+                   cudaMemcpyHostToDevice, I.up_stream, w);
+            ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(s, done, 0), "cudaStreamWaitEvent");
+            return;
+        }
+        const float* host = pc.is_a ? A : B;
         float* stage = elem == 0 ? reinterpret_cast<float*>(typed) : reinterpret_cast<float*>(base + f32_in[which]);
         copy2d(stage + r.off, host + r.off, r, cudaMemcpyHostToDevice, I.up_stream);
         ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
@@ -440,21 +560,15 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
         copy2d(C + cr.off, result + cr.off, cr, cudaMemcpyDeviceToHost, I.down_stream);
         ++ng;
     };
-    const double a_piece = 4.0 * mc * K, b_piece = 4.0 * K * nc;
-    int ia = 0, ib = 0;
-    std::vector<char> order;
-    while (ia < P || ib < Q) {
-        const bool take_a = ib == Q || (ia < P && ia * a_piece <= ib * b_piece);
-        if (take_a) {
-            upload(0, A, a_region(ia * mc, (ia + 1) * mc), ea, wa, ev_up[ia + ib]);
+    for (int i = 0, ia = 0, ib = 0, j = 0; i < np; ++i) {
+        for (; j < panel_end[static_cast<size_t>(i)]; ++j) upload(pieces[static_cast<size_t>(j)], ev_up[j]);
+        if (order[static_cast<size_t>(i)] == 'A') {
             ++ia;
             if (ib > 0) gemm((ia - 1) * mc, ia * mc, 0, ib * nc);
         } else {
-            upload(1, B, b_region(ib * nc, (ib + 1) * nc), eb, wb, ev_up[ia + ib]);
             ++ib;
             if (ia > 0) gemm(0, ia * mc, (ib - 1) * nc, ib * nc);
         }
-        order.push_back(take_a ? 'A' : 'B');
     }
     ck(cudaEventRecord(ev_down, I.down_stream), "cudaEventRecord");
     ck(cudaStreamWaitEvent(s, ev_down, 0), "cudaStreamWaitEvent");
@@ -471,8 +585,12 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
             cudaEventElapsedTime(&ms, ev_start, e);
             return ms;
         };
-        std::fprintf(stderr, "blocked %dx%d panels: up", P, Q);
-        for (int i = 0; i < np; ++i) std::fprintf(stderr, " %c%.3f", order[static_cast<size_t>(i)], at(ev_up[i]));
+        std::fprintf(stderr, "blocked %dx%d panels, %d pieces (%d host workers): up", P, Q, npc,
+                     pool ? pool->workers() : -1);
+        for (int j = 0; j < npc; ++j) {
+            const Piece& pc = pieces[static_cast<size_t>(j)];
+            std::fprintf(stderr, " %c%d%s%.3f", pc.is_a ? 'A' : 'B', pc.panel, pc.job ? "h" : "", at(ev_up[j]));
+        }
         std::fprintf(stderr, " | gemm");
         for (int g = 0; g < ng; ++g) std::fprintf(stderr, " %.3f-%.3f", at(ev_g[2 * g]), at(ev_g[2 * g + 1]));
         std::fprintf(stderr, " | C down done %.3f\n", at(ev_down));

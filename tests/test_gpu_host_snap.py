@@ -1,0 +1,71 @@
+"""Host snapping on the GPU box: fi_host_snap_f32 (host cores) against
+fi_convert_f32 (the device conversion, runtime/convert.cu) bit for bit, and
+fi_plan_run_host with host-snapped panels against the same call with every
+panel snapped on the device (FI_HOST_SNAP_SKIP past the panel count): the
+output must be bit-identical, including inputs beyond the f16 range that the
+reference saturates (anvil::round_to_f16, matrix.hpp:67-80)."""
+import re
+
+import numpy as np
+import pytest
+
+from test_host_snap import SPECIALS, payload_nans
+
+pytestmark = pytest.mark.gpu
+
+
+def device_convert(fi, x, code):
+    import torch
+    src = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+    dst = torch.empty(src.numel(), dtype=torch.int16, device="cuda")
+    fi._native.check(fi.lib.fi_convert_f32(src.data_ptr(), dst.data_ptr(), src.numel(), code,
+                                           torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    return dst.cpu().numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("elem,code", [("f16", 1), ("bf16", 2)])
+def test_host_snap_equals_device_conversion(fi, elem, code):
+    rng = np.random.default_rng(7)
+    bits = rng.integers(0, 2**32, size=1 << 20, dtype=np.uint64).astype(np.uint32).view(np.float32)
+    x = np.concatenate([SPECIALS, -SPECIALS, payload_nans(), bits,
+                        rng.uniform(-70000, 70000, 4096).astype(np.float32)])
+    np.testing.assert_array_equal(fi.host_snap(x, elem), device_convert(fi, x, code))
+
+
+CASES = [
+    (1024, 2048, 1024, dict(pair=True, tile_n=256)),
+    (1024, 2048, 2048, dict(pair=True, tile_n=128, ab="bf16")),
+    (1024, 2048, 1024, dict(pair=True, tile_n=256, layouts=("rowmajor", "colmajor", "colmajor"))),
+    (1024, 2048, 1024, dict(pair=True, tile_n=256, layouts=("colmajor", "rowmajor", "rowmajor"))),
+]
+
+
+@pytest.mark.parametrize("m,n,k,kw", CASES, ids=lambda x: str(x) if not isinstance(x, dict) else
+                         "_".join(f"{a}{b}" for a, b in x.items()))
+def test_run_host_host_snapped_panels_bit_identical(fi, oracle, monkeypatch, capfd, m, n, k, kw):
+    monkeypatch.setenv("FI_HOST_PANEL_MB", "1")
+    monkeypatch.setenv("FI_HOST_MIN_LINE", "128")
+    monkeypatch.setenv("FI_HOST_PIPELINE_TRACE", "1")
+    monkeypatch.delenv("FI_HOST_PIPELINE", raising=False)
+    plan = fi.Plan(fi.strategies.tc_strategy(m, n, k, **kw))
+    a = oracle.fill(m, k, 11, False) * np.float32(3.0)
+    b = oracle.fill(k, n, 12, False)
+    a[::97, ::89] = np.float32(70000.0)   # beyond f16: saturates to 65504 (f16 roots)
+    b[::61, ::53] = np.float32(-1e-7)     # f16 subnormal range
+    monkeypatch.setenv("FI_HOST_SNAP_SKIP", "1")
+    c_host = plan.run_host(a, b)
+    trace = capfd.readouterr().err
+    assert "blocked" in trace and re.search(r" [AB]\d+h", trace), trace  # pieces were host-snapped
+    monkeypatch.setenv("FI_HOST_SNAP_SKIP", "100000")
+    c_dev = plan.run_host(a, b)
+    trace = capfd.readouterr().err
+    assert "blocked" in trace and not re.search(r" [AB]\d+h", trace), trace
+    np.testing.assert_array_equal(c_host.view(np.uint32), c_dev.view(np.uint32))
+    # and exact against fp64 on integer inputs with host-snapped panels
+    monkeypatch.setenv("FI_HOST_SNAP_SKIP", "0")
+    ab = kw.get("ab", "f16")
+    a = oracle.fill(m, k, 3, True)
+    b = oracle.fill(k, n, 4, True)
+    want = oracle.gemm_f64(oracle.round_elem(a, ab), oracle.round_elem(b, ab))
+    assert np.array_equal(plan.run_host(a, b), want)
