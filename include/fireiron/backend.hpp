@@ -125,6 +125,8 @@ public:
     // elements each; pinned memory makes the copies asynchronous DMA).
     // Returns the kernel time in ms.
     double run_host_raw(const float* A, const float* B, float* C, void* stream = nullptr) const;
+    // bytes the last run_host moved host -> device and device -> host
+    void last_host_bytes(long& up, long& down) const;
 
     const PlanInfo& info() const;
     const Program& program() const;

@@ -101,6 +101,10 @@ fi_status fi_plan_launch_gated(fi_plan plan, const void* dA, const void* dB, voi
  * copies in, executes, copies the fp32 result out, synchronous. */
 fi_status fi_plan_run_host(fi_plan plan, const float* A, const float* B, float* C);
 
+/* Bytes the plan's last fi_plan_run_host moved host -> device and device ->
+ * host (host-snapped input pieces cross in 2-byte elements). */
+fi_status fi_plan_host_bytes(fi_plan plan, int64_t* h2d, int64_t* d2h);
+
 fi_status fi_plan_query(fi_plan plan, fi_plan_info* info);
 
 /* Generated CUDA translation unit for the plan (anvil::generate analogue,

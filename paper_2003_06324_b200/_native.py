@@ -89,6 +89,7 @@ def _load() -> C.CDLL:
     optional = {
         "fi_plan_create": ([C.c_char_p, i64, i64, i64, C.c_int, C.c_uint32, C.POINTER(vp)], C.c_int),
         "fi_plan_launch": ([vp, vp, vp, vp, vp], C.c_int),
+        "fi_plan_host_bytes": ([vp, C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "fi_plan_launch_gated": ([vp, vp, vp, vp, vp, vp, C.c_uint32, i64, i32], C.c_int),
         "fi_stream_write_u32": ([vp, C.c_uint32, vp], C.c_int),
         "fi_plan_run_host": ([vp, vp, vp, vp], C.c_int),

@@ -208,6 +208,12 @@ class Plan:
                                        out.ctypes.data))
         return out if c_row else out.T.copy()
 
+    def host_bytes(self):
+        """(H2D, D2H) bytes the last run_host moved across PCIe."""
+        up, down = C.c_int64(), C.c_int64()
+        N.check(N.lib.fi_plan_host_bytes(self._h, C.byref(up), C.byref(down)))
+        return int(up.value), int(down.value)
+
     def run_host_ptr(self, pA: int, pB: Optional[int], pC: int) -> None:
         """fi_plan_run_host on raw host pointers (physical root layouts, fp32)."""
         N.check(N.lib.fi_plan_run_host(self._h, C.c_void_p(pA), C.c_void_p(pB) if pB else None,

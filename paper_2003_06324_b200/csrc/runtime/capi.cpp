@@ -101,6 +101,17 @@ fi_status fi_plan_run_host(fi_plan plan, const float* A, const float* B, float* 
     });
 }
 
+fi_status fi_plan_host_bytes(fi_plan plan, int64_t* h2d, int64_t* d2h) {
+    if (!plan || !h2d || !d2h) return rt::set_error(FI_ERR_ARGUMENT, "fi_plan_host_bytes: null argument");
+    return guarded([&] {
+        long up = 0, down = 0;
+        plan->plan->last_host_bytes(up, down);
+        *h2d = up;
+        *d2h = down;
+        return FI_OK;
+    });
+}
+
 fi_status fi_plan_query(fi_plan plan, fi_plan_info* info) {
     if (!plan || !info) return rt::set_error(FI_ERR_ARGUMENT, "fi_plan_query: null argument");
     return guarded([&] {

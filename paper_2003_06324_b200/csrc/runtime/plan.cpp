@@ -276,6 +276,8 @@ struct Plan::Impl {
     // pinned host staging of host-snapped inputs (typed layout of each root)
     mutable void* host_stage = nullptr;
     mutable size_t host_stage_bytes = 0;
+    // bytes the last run_host moved across PCIe (host -> device, device -> host)
+    mutable long last_up = 0, last_down = 0;
 
     ~Impl() {
         if (module) {
@@ -521,6 +523,7 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
             pool->wait(pc.job.get());
             copy2d(typed + static_cast<size_t>(r.off) * w, reinterpret_cast<const char*>(pc.job->dst), r,
                    cudaMemcpyHostToDevice, I.up_stream, w);
+            I.last_up += r.width * r.height * static_cast<long>(w);
             ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
             ck(cudaStreamWaitEvent(s, done, 0), "cudaStreamWaitEvent");
             return;
@@ -528,6 +531,7 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
         const float* host = pc.is_a ? A : B;
         float* stage = elem == 0 ? reinterpret_cast<float*>(typed) : reinterpret_cast<float*>(base + f32_in[which]);
         copy2d(stage + r.off, host + r.off, r, cudaMemcpyHostToDevice, I.up_stream);
+        I.last_up += r.width * r.height * 4;
         ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
         ck(cudaStreamWaitEvent(s, done, 0), "cudaStreamWaitEvent");
         if (elem != 0)
@@ -558,6 +562,7 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
         ck(cudaEventRecord(ev_c[ng], s), "cudaEventRecord");
         ck(cudaStreamWaitEvent(I.down_stream, ev_c[ng], 0), "cudaStreamWaitEvent");
         copy2d(C + cr.off, result + cr.off, cr, cudaMemcpyDeviceToHost, I.down_stream);
+        I.last_down += cr.width * cr.height * 4;
         ++ng;
     };
     for (int i = 0, ia = 0, ib = 0, j = 0; i < np; ++i) {
@@ -638,6 +643,7 @@ double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, f
                                  : reinterpret_cast<float*>(base + f32_in[which]) + e0;
         ck(cudaMemcpyAsync(stage, host + e0, static_cast<size_t>(e1 - e0) * 4, cudaMemcpyHostToDevice, I.up_stream),
            "cudaMemcpyAsync");
+        I.last_up += (e1 - e0) * 4;
         ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
         ck(cudaStreamWaitEvent(s, done, 0), "cudaStreamWaitEvent");
         if (elem != 0)  // snapping to the root's element grid on ingestion (sim.hpp:507-510)
@@ -676,6 +682,7 @@ double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, f
         ck(cudaStreamWaitEvent(I.down_stream, ev_c[j], 0), "cudaStreamWaitEvent");
         ck(cudaMemcpyAsync(C + c0, result, static_cast<size_t>(c1 - c0) * 4, cudaMemcpyDeviceToHost, I.down_stream),
            "cudaMemcpyAsync");
+        I.last_down += (c1 - c0) * 4;
     }
     ck(cudaEventRecord(ev_down, I.down_stream), "cudaEventRecord");
     ck(cudaStreamWaitEvent(s, ev_down, 0), "cudaStreamWaitEvent");
@@ -707,6 +714,11 @@ double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, f
 Plan::Plan(std::unique_ptr<Impl> impl) : impl_(std::move(impl)) {}
 Plan::~Plan() = default;
 const PlanInfo& Plan::info() const { return impl_->info; }
+void Plan::last_host_bytes(long& up, long& down) const {
+    std::lock_guard<std::mutex> g(impl_->mu);
+    up = impl_->last_up;
+    down = impl_->last_down;
+}
 const Program& Plan::program() const { return impl_->prog; }
 const std::string& Plan::source() const { return impl_->source; }
 
@@ -925,6 +937,7 @@ double Plan::run_host_raw(const float* A, const float* B, float* C, void* stream
         I.scratch_bytes = off;
     }
     auto* base = static_cast<char*>(I.scratch);
+    I.last_up = I.last_down = 0;
     if (!I.ev0) {
         ck(cudaEventCreate(&I.ev0), "cudaEventCreate");
         ck(cudaEventCreate(&I.ev1), "cudaEventCreate");
@@ -935,6 +948,7 @@ double Plan::run_host_raw(const float* A, const float* B, float* C, void* stream
         return run_host_pipelined(I, A, B, C, s, chunks, base, f32_in, typed_in, typed_c, f32_c);
     for (int i = 0; i < nin; ++i) {
         const BufferDecl& r = I.root(i);
+        I.last_up += r.extent() * 4;
         if (r.elem == ElemType::F32) {  // copy straight into the typed buffer
             ck(cudaMemcpyAsync(base + typed_in[i], ins[i], static_cast<size_t>(r.extent()) * 4,
                                cudaMemcpyHostToDevice, s),
@@ -960,6 +974,7 @@ double Plan::run_host_raw(const float* A, const float* B, float* C, void* stream
     }
     ck(cudaMemcpyAsync(C, result, static_cast<size_t>(out.extent()) * 4, cudaMemcpyDeviceToHost, s),
        "cudaMemcpyAsync");
+    I.last_down = out.extent() * 4;
     ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     float ms = 0.f;
     cudaEventElapsedTime(&ms, I.ev0, I.ev1);

@@ -57,10 +57,13 @@ def test_run_host_host_snapped_panels_bit_identical(fi, oracle, monkeypatch, cap
     c_host = plan.run_host(a, b)
     trace = capfd.readouterr().err
     assert "blocked" in trace and re.search(r" [AB]\d+h", trace), trace  # pieces were host-snapped
+    up, down = plan.host_bytes()  # host-snapped pieces cross PCIe in 2-byte elements
+    assert down == 4 * m * n and 2 * (m * k + k * n) <= up < 4 * (m * k + k * n), (up, down)
     monkeypatch.setenv("FI_HOST_SNAP_SKIP", "100000")
     c_dev = plan.run_host(a, b)
     trace = capfd.readouterr().err
     assert "blocked" in trace and not re.search(r" [AB]\d+h", trace), trace
+    assert plan.host_bytes() == (4 * (m * k + k * n), 4 * m * n)
     np.testing.assert_array_equal(c_host.view(np.uint32), c_dev.view(np.uint32))
     # and exact against fp64 on integer inputs with host-snapped panels
     monkeypatch.setenv("FI_HOST_SNAP_SKIP", "0")
