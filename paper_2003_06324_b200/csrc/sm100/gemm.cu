@@ -80,17 +80,39 @@ struct DeviceState {
 };
 constexpr int kMaxDevices = 64;
 
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1, int kMcast = 1>
+CUresult encode_nd(CUtensorMap* map, CUtensorMapDataType dt, const void* base, int rank, const cuuint64_t* dims,
+                   const cuuint64_t* strides, const cuuint32_t* box) {
+    EncodeTiledFn encode = encode_tiled_fn();
+    if (!encode) return CUDA_ERROR_NOT_INITIALIZED;
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    return encode(map, dt, rank, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1, int kMcast = 1, int kKB = 1>
 int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t stream, bool dry_run = false) {
-    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
-    auto kernel = fi_sm100_gemm<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kMcast>;
+    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kKB>;
+    auto kernel = fi_sm100_gemm<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kMcast, kKB>;
     constexpr int kCluster = kCtaGroup * kSplitK * kMcast;
 
     const CUtensorMapDataType dt =
         cfg.ab_format == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     CUtensorMap tmA, tmB, tmB2, tmC, tmC2;
     CUresult r;
-    if (cfg.a_mn_major && kMcast == 1) {
+    const cuuint64_t kblocks = static_cast<cuuint64_t>(p.K / 64);
+    if (kKB == 2 && cfg.a_mn_major) {
+        // (64 rows, 64 k, M/64 panels, K/64 blocks): box {64, 64, 2, 2} = both panels of two K blocks
+        cuuint64_t dims[4] = {64, 64, static_cast<cuuint64_t>(p.M / 64), kblocks};
+        cuuint64_t strides[3] = {static_cast<cuuint64_t>(p.lda) * 2, 128, static_cast<cuuint64_t>(p.lda) * 128};
+        cuuint32_t box[4] = {64, 64, 2, 2};
+        r = encode_nd(&tmA, dt, p.A, 4, dims, strides, box);
+    } else if (kKB == 2) {
+        // K-major: (64 k, M rows, K/64 blocks): box {64, 128, 2}
+        cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(p.M), kblocks};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.lda) * 2, 128};
+        cuuint32_t box[3] = {64, static_cast<cuuint32_t>(S::BM), 2};
+        r = encode_nd(&tmA, dt, p.A, 3, dims, strides, box);
+    } else if (cfg.a_mn_major && kMcast == 1) {
         // (64 rows, K, M/64 panels): box {64, 64, 2} = one slab's two SW128 panels
         EncodeTiledFn encode = encode_tiled_fn();
         cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(p.K), static_cast<cuuint64_t>(p.M / 64)};
@@ -106,14 +128,29 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
     else
         r = encode_2d(&tmA, dt, p.A, p.K, p.M, static_cast<uint64_t>(p.lda) * 2, 64, kMcast > 1 ? 64 : S::BM);
     if (r != CUDA_SUCCESS) return kTcErrTensorMap;
-    if (cfg.b_mn_major)
+    if (cfg.b_mn_major) {
         r = encode_2d(&tmB, dt, p.B, p.N, p.K, static_cast<uint64_t>(p.ldb) * 2, 64, 64);
-    else
+    } else if (kKB == 2) {
+        // K-major: (64 k, N rows, K/64 blocks): box {64, BN_LOCAL, 2}
+        cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(p.N), kblocks};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.ldb) * 2, 128};
+        cuuint32_t box[3] = {64, static_cast<cuuint32_t>(S::BN_LOCAL), 2};
+        r = encode_nd(&tmB, dt, p.B, 3, dims, strides, box);
+    } else {
         r = encode_2d(&tmB, dt, p.B, p.K, p.N, static_cast<uint64_t>(p.ldb) * 2, 64, S::BN_LOCAL);
-    if (r == CUDA_SUCCESS && !cfg.b_mn_major && S::BN_LOCAL >= 16)  // half-width tail units
-        r = encode_2d(&tmB2, dt, p.B, p.K, p.N, static_cast<uint64_t>(p.ldb) * 2, 64, S::BN_LOCAL / 2);
-    else
+    }
+    if (r == CUDA_SUCCESS && !cfg.b_mn_major && S::BN_LOCAL >= 16) {  // half-width tail units
+        if (kKB == 2) {
+            cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(p.N), kblocks};
+            cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.ldb) * 2, 128};
+            cuuint32_t box[3] = {64, static_cast<cuuint32_t>(S::BN_LOCAL / 2), 2};
+            r = encode_nd(&tmB2, dt, p.B, 3, dims, strides, box);
+        } else {
+            r = encode_2d(&tmB2, dt, p.B, p.K, p.N, static_cast<uint64_t>(p.ldb) * 2, 64, S::BN_LOCAL / 2);
+        }
+    } else {
         tmB2 = tmB;
+    }
     if (r != CUDA_SUCCESS) return kTcErrTensorMap;
     // f32 column-major C: the epilogue stages 128x32 chunks in smem and stores
     // them with one TMA bulk tensor store each (FI_TC_CSTORE=0 disables)
@@ -422,6 +459,14 @@ int tc_gemm_launch(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t
     // grown and its epoch advanced under the pool lock
     std::unique_lock<std::mutex> pool_lock(pool_mutex(), std::defer_lock);
     if (!p.workspace && !dry_run) pool_lock.lock();
+    // FI_TC_KB=2: two-K-block stages (half the TMA operations) for the pair 256 x 256 tile
+    static const int kb_env = [] {
+        const char* v = std::getenv("FI_TC_KB");
+        return v ? std::atoi(v) : 1;
+    }();
+    if (kb_env == 2 && cfg.cta_group == 2 && cfg.bn == 256 && cfg.split_k == 1 && cfg.slabs == 1 &&
+        cfg.n_halves == 1 && cfg.mcast == 1)
+        return launch_impl<2, 256, 1, 1, 1, 1, 2>(cfg, p, stream, dry_run);
     if (cfg.slabs == 2) return launch_impl<2, 256, 1, 2>(cfg, p, stream, dry_run);
     if (cfg.n_halves == 2) return launch_impl<2, 256, 1, 1, 2>(cfg, p, stream, dry_run);
     if (cfg.mcast == 2) {

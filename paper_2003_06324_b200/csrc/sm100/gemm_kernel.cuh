@@ -115,12 +115,13 @@ __device__ __forceinline__ void epilogue_bar() { asm volatile("bar.sync 1, 128;"
 
 // Kernel body; the tensor maps must be __grid_constant__ kernel parameters
 // (TMA reads them through their parameter-space address).
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves, int kMcast>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves, int kMcast, int kKB>
 __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                                    const CUtensorMap& tmB2, const CUtensorMap& tmC,
                                                    const CUtensorMap& tmC2,
                                                    const GemmArgs& args) {
-    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves>;
+    using S = GemmShape<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kKB>;
+    static_assert(kKB == 1 || (kKB == 2 && kMcast == 1), "two-K-block stages: not with multicast");
     static_assert(kSlabs * kNHalves == 1 || (kCtaGroup == 2 && kSplitK == 1 && kSlabs * kNHalves == 2),
                   "slab / N-half tiles pair with CTA pairs, one doubling, no cluster split-K");
     constexpr bool kWide = kSlabs * kNHalves > 1;  // whole-TMEM accumulator, whole-tile units only
@@ -229,11 +230,14 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 const int m0 = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
                 const int n0 = tn * kBNTile + static_cast<int>(mc_rank) * S::BN_TILE + u.n_off +
                                static_cast<int>(pair_rank) * b_rows;
-                for (int kb = u.k0; kb < u.k1; ++kb) {
+                for (int kb = u.k0; kb < u.k1; kb += kKB) {
                     mbar_wait(&empty_bar[s], ph ^ 1);
                     uint8_t* sa = ring + s * S::STAGE_BYTES;
-                    uint8_t* sb = sa + S::A_BYTES;
+                    uint8_t* sb = sa + S::A_STAGE_BYTES;
                     const int k0 = (kb0 + kb) * S::BK;
+                    // kKB = 2: the box covers two K blocks even when the unit has one
+                    // left (the second is read but not multiplied; past K it is zero-
+                    // filled); the transaction count is the full box either way
                     if (mma_leader) mbar_arrive_expect_tx(&full_bar[s], tx);
                     auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol) {
                         if (args.l2_hint) {
@@ -243,6 +247,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                             if constexpr (kCtaGroup == 1) tma_load_2d(dst, map, &full_bar[s], c0, c1);
                             else tma_load_2d_pair(dst, map, &full_bar[s], c0, c1);
                         }
+                    };
+                    auto load3 = [&](void* dst, const CUtensorMap* map, int c0, int c1, int c2) {
+                        if constexpr (kCtaGroup == 1) tma_load_3d(dst, map, &full_bar[s], c0, c1, c2);
+                        else tma_load_3d_pair(dst, map, &full_bar[s], c0, c1, c2);
                     };
                     if constexpr (kMcast > 1) {
                         // my 64-row half of the A block, to me and my rank-twin in the other pair
@@ -254,14 +262,22 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     } else {
 #pragma unroll
                         for (int sl = 0; sl < kSlabs; ++sl) {  // slab sl: rows m0 + sl * BM_MMA
-                            uint8_t* sas = sa + sl * S::SLAB_BYTES;
+                            uint8_t* sas = sa + sl * kKB * S::SLAB_BYTES;
                             const int m0s = m0 + sl * S::BM_MMA;
-                            if (args.a_mn_major) {
+                            if constexpr (kKB == 2) {
+                                // one box for both K blocks: MN-major {64, 64, 2 panels, 2 K blocks},
+                                // K-major {64 k, 128 rows, 2 K blocks}
+                                if (args.a_mn_major) {
+                                    if constexpr (kCtaGroup == 1) tma_load_4d(sas, &tmA, &full_bar[s], 0, 0, m0s / 64, kb0 + kb);
+                                    else tma_load_4d_pair(sas, &tmA, &full_bar[s], 0, 0, m0s / 64, kb0 + kb);
+                                } else {
+                                    load3(sas, &tmA, 0, m0s, kb0 + kb);
+                                }
+                            } else if (args.a_mn_major) {
                                 // one 3D box {64, 64, 2}: both 64-row SW128 panels of the slab
                                 // (tmA viewed as 64 rows x K x M/64 panels) -- one TMA op instead
                                 // of two; the SM's TMA unit is a bottleneck of the main loop
-                                if constexpr (kCtaGroup == 1) tma_load_3d(sas, &tmA, &full_bar[s], 0, k0, m0s / 64);
-                                else tma_load_3d_pair(sas, &tmA, &full_bar[s], 0, k0, m0s / 64);
+                                load3(sas, &tmA, 0, k0, m0s / 64);
                             } else {
                                 load(sas, &tmA, k0, m0s, pol_a);
                             }
@@ -269,11 +285,14 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     }
 #pragma unroll
                     for (int h = 0; h < kNHalves; ++h) {  // N half h: rows n0 + h * BN
-                        uint8_t* sbh = sb + h * S::HALF_B_BYTES;
+                        uint8_t* sbh = sb + h * kKB * S::HALF_B_BYTES;
                         const int n0h = n0 + h * BN;
                         if (args.b_mn_major) {
-                            for (int j = 0; j < b_rows / 64; ++j)
-                                load(sbh + j * 8192, &tmB, n0h + j * 64, k0, pol_b);
+                            for (int b = 0; b < kKB; ++b)
+                                for (int j = 0; j < b_rows / 64; ++j)
+                                    load(sbh + b * b_rows * 128 + j * 8192, &tmB, n0h + j * 64, k0 + b * S::BK, pol_b);
+                        } else if constexpr (kKB == 2) {
+                            load3(sbh, half ? &tmB2 : &tmB, 0, n0h, kb0 + kb);
                         } else {
                             load(sbh, half ? &tmB2 : &tmB, k0, n0h, pol_b);  // tmB2: box of BN_LOCAL/2 rows
                         }
@@ -309,28 +328,35 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 mbar_wait_cluster(&tempty_bar[buf], (use & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * S::ACC_COLS);
-                for (int kb = u.k0; kb < u.k1; ++kb) {
+                const uint32_t b_kb_bytes = static_cast<uint32_t>(u.width / kCtaGroup) * 128;  // B rows x 128 B
+                for (int kb = u.k0; kb < u.k1; kb += kKB) {
                     mbar_wait(&full_bar[s], ph);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(ring + s * S::STAGE_BYTES);
-                    const uint32_t sb = sa + S::A_BYTES;
+                    const uint32_t sb = sa + S::A_STAGE_BYTES;
 #pragma unroll
-                    for (int k = 0; k < S::BK / 16; ++k) {
-                        const uint32_t acc = (kb > u.k0 || k > 0) ? 1u : 0u;
-                        if constexpr (kNHalves == 2) {
-                            // two N halves share A: the first MMA fills the A collector,
-                            // the second reuses it (A leaves shared memory once)
-                            uint64_t ad = smem_desc_sw128(sa + k * a_kstep, a_lbo, 1024);
-                            uint64_t bd0 = smem_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
-                            uint64_t bd1 = smem_desc_sw128(sb + S::HALF_B_BYTES + k * b_kstep, b_lbo, 1024);
-                            umma_f16_collect<kCtaGroup, 1>(d_tmem, ad, bd0, idesc, acc);
-                            umma_f16_collect<kCtaGroup, 2>(d_tmem + BN, ad, bd1, idesc, acc);
-                        } else {
-                            uint64_t bd = smem_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
+                    for (int b = 0; b < kKB; ++b) {
+                        if (kKB > 1 && kb + b >= u.k1) break;  // a unit's odd last K block
 #pragma unroll
-                            for (int sl = 0; sl < kSlabs; ++sl) {  // slabs share the B operand
-                                uint64_t ad = smem_desc_sw128(sa + sl * S::SLAB_BYTES + k * a_kstep, a_lbo, 1024);
-                                umma_f16<kCtaGroup>(d_tmem + sl * BN, ad, bd, idesc, acc);
+                        for (int k = 0; k < S::BK / 16; ++k) {
+                            const uint32_t acc = (kb > u.k0 || b > 0 || k > 0) ? 1u : 0u;
+                            if constexpr (kNHalves == 2) {
+                                // two N halves share A: the first MMA fills the A collector,
+                                // the second reuses it (A leaves shared memory once)
+                                uint64_t ad = smem_desc_sw128(sa + b * S::SLAB_BYTES + k * a_kstep, a_lbo, 1024);
+                                uint64_t bd0 = smem_desc_sw128(sb + b * b_kb_bytes + k * b_kstep, b_lbo, 1024);
+                                uint64_t bd1 = smem_desc_sw128(sb + kKB * S::HALF_B_BYTES + b * b_kb_bytes + k * b_kstep,
+                                                               b_lbo, 1024);
+                                umma_f16_collect<kCtaGroup, 1>(d_tmem, ad, bd0, idesc, acc);
+                                umma_f16_collect<kCtaGroup, 2>(d_tmem + BN, ad, bd1, idesc, acc);
+                            } else {
+                                uint64_t bd = smem_desc_sw128(sb + b * b_kb_bytes + k * b_kstep, b_lbo, 1024);
+#pragma unroll
+                                for (int sl = 0; sl < kSlabs; ++sl) {  // slabs share the B operand
+                                    uint64_t ad = smem_desc_sw128(
+                                        sa + (sl * kKB + b) * S::SLAB_BYTES + k * a_kstep, a_lbo, 1024);
+                                    umma_f16<kCtaGroup>(d_tmem + sl * BN, ad, bd, idesc, acc);
+                                }
                             }
                         }
                     }
@@ -793,13 +819,13 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     }
 }
 
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves, int kMcast = 1>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves, int kMcast = 1, int kKB = 1>
 __global__ void __launch_bounds__(256, 1)
     fi_sm100_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
                   const __grid_constant__ CUtensorMap tmC2,
                   const __grid_constant__ GemmArgs args) {
-    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kMcast>(tmA, tmB, tmB2, tmC, tmC2, args);
+    fi_sm100_gemm_body<kCtaGroup, BN, kSplitK, kSlabs, kNHalves, kMcast, kKB>(tmA, tmB, tmB2, tmC, tmC2, args);
 }
 
 }  // namespace fireiron::sm100

@@ -82,7 +82,11 @@ struct GemmArgs {
 // kNHalves = 2 (same restrictions): the pair computes 256 x 512 with two
 // N = 256 MMAs per K step sharing A through the tensor core's A collector
 // (read from shared memory once), the B stage holding both N halves.
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1>
+// kKB = 2: a stage holds two 64-deep K blocks, loaded with one TMA box per
+// operand (a 3D/4D view whose outer dimension walks K blocks): half the TMA
+// operations of kKB = 1 for the same bytes. Stage layout: A [slab][kb][16 KiB],
+// B [N half][kb][b_rows * 128 B].
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs = 1, int kNHalves = 1, int kKB = 1>
 struct GemmShape {
     static constexpr int BM = 128;                 // rows per CTA and slab (TMEM lanes)
     static constexpr int BM_MMA = 128 * kCtaGroup; // rows of one MMA (a slab across the pair)
@@ -94,7 +98,9 @@ struct GemmShape {
     static constexpr int A_BYTES = SLAB_BYTES * kSlabs;
     static constexpr int HALF_B_BYTES = BN_LOCAL * BK * 2;
     static constexpr int B_BYTES = HALF_B_BYTES * kNHalves;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int KB_STAGE = kKB;             // K blocks per stage
+    static constexpr int A_STAGE_BYTES = A_BYTES * kKB;
+    static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * kKB;
     // split-K reduction scratch: the fp32 partial tile (rows padded by 16B)
     // reuses the operand ring once the tile's main loop has drained it
     static constexpr int RED_LD = BN + 4;
@@ -122,7 +128,9 @@ struct GemmShape {
     static constexpr int kThreads = 256;
     // transaction bytes one stage's TMA loads credit to the (leader's) full
     // barrier: A slabs + B halves of b_rows rows, from every CTA of the pair
-    static constexpr FI_HD int stage_tx_bytes(int b_rows) { return (A_BYTES + b_rows * BK * 2 * kNHalves) * kCtaGroup; }
+    static constexpr FI_HD int stage_tx_bytes(int b_rows) {
+        return (A_BYTES + b_rows * BK * 2 * kNHalves) * kCtaGroup * kKB;
+    }
     static constexpr int WS_FLOATS = BN * BM;     // one CTA's partial tile
 };
 
