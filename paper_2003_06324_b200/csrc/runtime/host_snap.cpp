@@ -109,15 +109,20 @@ PoolState& state() {
     return *s;
 }
 
+void line(const SnapJob* j, const float* src, long doff, long n) {
+    if (j->elem == 0) std::memcpy(static_cast<float*>(j->dst) + doff, src, static_cast<size_t>(n) * 4);
+    else snap_f32(src, static_cast<uint16_t*>(j->dst) + doff, n, j->elem);
+}
+
 void convert_piece(SnapJob* j, long p) {
     const long l0 = p * j->lines_per_piece;
     const long l1 = l0 + j->lines_per_piece < j->height ? l0 + j->lines_per_piece : j->height;
     if (j->height == 1) {  // one long line: pieces are element ranges
         const long e0 = p * kPieceElems, e1 = e0 + kPieceElems < j->width ? e0 + kPieceElems : j->width;
-        snap_f32(j->src + e0, j->dst + e0, e1 - e0, j->elem);
+        line(j, j->src + e0, e0, e1 - e0);
         return;
     }
-    for (long l = l0; l < l1; ++l) snap_f32(j->src + l * j->spitch, j->dst + l * j->dpitch, j->width, j->elem);
+    for (long l = l0; l < l1; ++l) line(j, j->src + l * j->spitch, l * j->dpitch, j->width);
 }
 
 }  // namespace

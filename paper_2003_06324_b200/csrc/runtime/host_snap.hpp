@@ -19,12 +19,13 @@
 namespace fireiron::rt {
 
 // One 2D region: `height` lines of `width` elements, line i at src + i * spitch
-// (floats) and dst + i * dpitch (elements of the 2-byte target type).
+// (floats) and dst + i * dpitch (elements of the target type). elem 0 copies
+// fp32 (staging a pageable result into / out of pinned memory).
 struct SnapJob {
     const float* src = nullptr;
-    uint16_t* dst = nullptr;
+    void* dst = nullptr;
     long width = 0, height = 0, spitch = 0, dpitch = 0;
-    int elem = 1;  // 1 f16, 2 bf16
+    int elem = 1;  // 0 f32 copy, 1 f16, 2 bf16
     // filled by the pool
     long lines_per_piece = 0, npieces = 0;
     std::atomic<long> next{0}, done{0};

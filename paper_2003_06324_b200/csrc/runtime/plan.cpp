@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <algorithm>
 #include <map>
 #include <memory>
@@ -276,6 +277,9 @@ struct Plan::Impl {
     // pinned host staging of host-snapped inputs (typed layout of each root)
     mutable void* host_stage = nullptr;
     mutable size_t host_stage_bytes = 0;
+    mutable void* host_cstage = nullptr;  // pinned staging of a pageable C
+    mutable size_t host_cstage_bytes = 0;
+    mutable std::vector<cudaEvent_t> hev;  // host pipeline: C region landed (staged C)
     // bytes the last run_host moved across PCIe (host -> device, device -> host)
     mutable long last_up = 0, last_down = 0;
 
@@ -293,6 +297,8 @@ struct Plan::Impl {
         if (down_stream) cudaStreamDestroy(down_stream);
         for (cudaEvent_t e : pev) cudaEventDestroy(e);
         if (host_stage) cudaFreeHost(host_stage);
+        if (host_cstage) cudaFreeHost(host_cstage);
+        for (cudaEvent_t e : hev) cudaEventDestroy(e);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
     }
@@ -372,6 +378,263 @@ bool blocked_split(const Plan::Impl& I, int& P, int& Q) {
     return P * Q >= 4;
 }
 
+// ---------------------------------------------------------------- host side of both pipelines
+// Uploads: each input region is cut into pieces of whole lines (~FI_HOST_PIECE_MB
+// of fp32, default 8). Host snapping (runtime/host_snap.hpp): a fraction
+// FI_HOST_SNAP_RATIO (default 0.8) of the pieces of f16/bf16 roots, spread
+// evenly over the upload order, is converted by host cores into pinned staging
+// while the copy engine moves the others as fp32 (snapped on the device), and
+// then crosses PCIe in 2-byte elements. The ratio balances the two engines
+// measured on the B200 box: the copy engine moves ~54 GB/s, the host converts
+// ~60 GB/s of fp32 while the copy engine also reads host memory
+// (profiles/round2/host_snap_probe.txt, host_snap_e2e_ab.log). The first
+// FI_HOST_SNAP_SKIP pieces (default 1) are snapped on the device so the copy
+// engine starts at once. Pageable inputs (anvil::Matrix is a std::vector) are
+// snapped on the host entirely: the driver's staged pageable copies are slower
+// than the host conversion. A piece is either converted on the host or uploaded
+// as fp32, never both: once many host threads have read a pinned buffer the copy
+// engine reads it at ~60 % speed (profiles/round2/dma_after_cpu_read.txt).
+// Downloads: C regions go down on the down stream; a pageable C is staged in
+// pinned memory and copied out by the host pool as each region lands.
+struct HostIO {
+    struct Piece {
+        int which;  // 0 A, 1 B
+        int tag;    // caller's label (panel index) for the trace
+        Region r;
+        std::unique_ptr<rt::SnapJob> job;
+    };
+    struct Down {
+        Region r;
+        cudaEvent_t ev;
+        std::unique_ptr<rt::SnapJob> job;
+    };
+
+    const Plan::Impl& I;
+    cudaStream_t s;
+    char* base;
+    const size_t* f32_in;
+    const size_t* typed_in;
+    const float* in[2];
+    float* C;
+    int elem[2];
+    size_t w[2];
+    rt::HostSnapPool* pool = nullptr;
+    bool pinned[2] = {true, true};
+    float* c_stage = nullptr;  // pinned staging of a pageable C
+    std::vector<Piece> pieces;
+    std::vector<Down> downs;
+    size_t nev = 0;
+
+    static bool is_pinned(const void* p) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    }
+
+    HostIO(const Plan::Impl& I_, cudaStream_t s_, char* base_, const size_t* f32_in_, const size_t* typed_in_,
+           const float* A, const float* B, float* C_)
+        : I(I_), s(s_), base(base_), f32_in(f32_in_), typed_in(typed_in_), in{A, B}, C(C_) {
+        for (int i = 0; i < 2; ++i) {
+            elem[i] = elem_code(I.root(i).elem);
+            w[i] = byte_width(I.root(i).elem);
+        }
+        if (elem[0] != 0 || elem[1] != 0 || !is_pinned(C)) pool = rt::HostSnapPool::get();
+        if (pool) {
+            pinned[0] = is_pinned(A);
+            pinned[1] = is_pinned(B);
+            if (!is_pinned(C)) {
+                const size_t cbytes = static_cast<size_t>(I.root(I.out_root()).extent()) * 4;
+                if (I.host_cstage_bytes < cbytes) {
+                    if (I.host_cstage) cudaFreeHost(I.host_cstage);
+                    I.host_cstage = nullptr;
+                    I.host_cstage_bytes = 0;
+                    ck(cudaHostAlloc(&I.host_cstage, cbytes, cudaHostAllocPortable), "cudaHostAlloc");
+                    I.host_cstage_bytes = cbytes;
+                }
+                c_stage = static_cast<float*>(I.host_cstage);
+            }
+        }
+    }
+    // every submitted job is waited for, also when an enqueue throws: the pool's
+    // workers must not touch a job (or the caller's buffers) after we return
+    ~HostIO() {
+        if (!pool) return;
+        for (auto& p : pieces)
+            if (p.job) pool->wait(p.job.get());
+        for (auto& d : downs)
+            if (d.job) pool->wait(d.job.get());
+    }
+
+    cudaEvent_t event() {
+        if (nev == I.hev.size()) {
+            cudaEvent_t e;
+            ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            I.hev.push_back(e);
+        }
+        return I.hev[nev++];
+    }
+
+    // cut region r of input `which` into pieces of whole lines; returns one past the last
+    int add(int which, const Region& r, int tag) {
+        double piece_bytes = 8.0 * (1 << 20);
+        if (const char* v = std::getenv("FI_HOST_PIECE_MB")) piece_bytes = std::atof(v) * (1 << 20);
+        long nsub = std::max(1L, std::lround(4.0 * r.width * r.height / piece_bytes));
+        if (r.width == r.pitch && r.height < nsub) {
+            // contiguous storage with few lines (a whole operand): cut element
+            // ranges on 1024-element boundaries
+            const long n = r.width * r.height;
+            for (long q = 0; q < nsub; ++q) {
+                const long e0 = (n * q / nsub) & ~1023L, e1 = q + 1 == nsub ? n : (n * (q + 1) / nsub) & ~1023L;
+                if (e1 > e0) pieces.push_back(Piece{which, tag, Region{r.off + e0, e1 - e0, 1, e1 - e0}, nullptr});
+            }
+            return static_cast<int>(pieces.size());
+        }
+        nsub = std::min(nsub, r.height);
+        for (long q = 0; q < nsub; ++q) {
+            const long l0 = r.height * q / nsub, l1 = r.height * (q + 1) / nsub;
+            pieces.push_back(Piece{which, tag, Region{r.off + l0 * r.pitch, r.width, l1 - l0, r.pitch}, nullptr});
+        }
+        return static_cast<int>(pieces.size());
+    }
+
+    // decide host / device snapping per piece and start the host conversions
+    void start() {
+        if (!pool || (elem[0] == 0 && elem[1] == 0)) return;
+        size_t hoff[2] = {0, 0}, hbytes = 0;
+        for (int i = 0; i < 2; ++i) {
+            hoff[i] = hbytes;
+            hbytes += (static_cast<size_t>(I.root(i).extent()) * 2 + 255) & ~size_t(255);
+        }
+        if (I.host_stage_bytes < hbytes) {
+            if (I.host_stage) cudaFreeHost(I.host_stage);
+            I.host_stage = nullptr;
+            I.host_stage_bytes = 0;
+            ck(cudaHostAlloc(&I.host_stage, hbytes, cudaHostAllocPortable), "cudaHostAlloc");
+            I.host_stage_bytes = hbytes;
+        }
+        // leading pieces snapped on the device: 1 for pinned inputs (the copy engine
+        // starts at once), none for pageable ones (their staged copies are slow)
+        int skip = -1;
+        if (const char* v = std::getenv("FI_HOST_SNAP_SKIP")) skip = std::atoi(v);
+        double ratio = 0.8;
+        if (const char* v = std::getenv("FI_HOST_SNAP_RATIO")) ratio = std::atof(v);
+        ratio = std::min(ratio, ratio * (pool->workers() + 1) / 16.0);  // fewer host threads convert less
+        const int npc = static_cast<int>(pieces.size());
+        for (int j = 0, h = 0; j < npc; ++j) {
+            Piece& pc = pieces[static_cast<size_t>(j)];
+            const int e = elem[pc.which];
+            if (e == 0) continue;
+            const int sk = skip >= 0 ? skip : pinned[pc.which] ? 1 : 0;
+            if (j < sk) continue;
+            bool host = !pinned[pc.which];  // pageable input: every piece
+            if (!host) {
+                // piece j - skip goes to the host when the running share crosses an integer
+                const int want = static_cast<int>(std::floor((j - skip + 1) * ratio + 1e-9));
+                host = want > h;
+                h = std::max(h, want);
+            }
+            if (!host) continue;
+            auto job = std::make_unique<rt::SnapJob>();
+            job->src = in[pc.which] + pc.r.off;
+            job->dst = reinterpret_cast<uint16_t*>(static_cast<char*>(I.host_stage) + hoff[pc.which]) + pc.r.off;
+            job->width = pc.r.width;
+            job->height = pc.r.height;
+            job->spitch = job->dpitch = pc.r.pitch;
+            job->elem = e;
+            if (pc.r.width == pc.r.pitch) {  // contiguous: one long line
+                job->width = pc.r.width * pc.r.height;
+                job->height = 1;
+            }
+            pc.job = std::move(job);
+        }
+        for (auto& pc : pieces)  // FIFO: converted in upload order
+            if (pc.job) pool->submit(pc.job.get());
+    }
+
+    static void copy2d(void* dst, const void* src, const Region& r, cudaMemcpyKind kind, cudaStream_t st, size_t w) {
+        if (r.width == r.pitch)  // contiguous lines: one linear copy
+            ck(cudaMemcpyAsync(dst, src, static_cast<size_t>(r.width * r.height) * w, kind, st), "cudaMemcpyAsync");
+        else
+            ck(cudaMemcpy2DAsync(dst, r.pitch * w, src, r.pitch * w, r.width * w, r.height, kind, st),
+               "cudaMemcpy2DAsync");
+    }
+
+    // one piece: H2D into the fp32 staging (or straight into an fp32 root), then
+    // snapped to the root's element grid on s (sim.hpp:507-510); or, when host
+    // snapped, H2D of the snapped piece straight into the typed root. `done` is
+    // recorded on the up stream and s waits for it.
+    void upload(int j, cudaEvent_t done) {
+        const Piece& pc = pieces[static_cast<size_t>(j)];
+        const int which = pc.which, e = elem[which];
+        const Region& r = pc.r;
+        char* typed = base + typed_in[which];
+        if (pc.job) {
+            pool->wait(pc.job.get());
+            copy2d(typed + static_cast<size_t>(r.off) * w[which], pc.job->dst, r, cudaMemcpyHostToDevice, I.up_stream,
+                   w[which]);
+            I.last_up += r.width * r.height * static_cast<long>(w[which]);
+        } else {
+            float* stage = e == 0 ? reinterpret_cast<float*>(typed) : reinterpret_cast<float*>(base + f32_in[which]);
+            copy2d(stage + r.off, in[which] + r.off, r, cudaMemcpyHostToDevice, I.up_stream, 4);
+            I.last_up += r.width * r.height * 4;
+        }
+        ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(s, done, 0), "cudaStreamWaitEvent");
+        if (!pc.job && e != 0) {
+            float* stage = reinterpret_cast<float*>(base + f32_in[which]);
+            ck(rt::convert_f32_2d(stage + r.off, typed + static_cast<size_t>(r.off) * w[which], r.width, r.height,
+                                  r.pitch, e, s),
+               "input conversion");
+        }
+    }
+
+    // D2H of C region cr from the fp32 device result (after `ready` on s)
+    void download(const float* result, const Region& cr, cudaEvent_t ready) {
+        ck(cudaStreamWaitEvent(I.down_stream, ready, 0), "cudaStreamWaitEvent");
+        copy2d((c_stage ? c_stage : C) + cr.off, result + cr.off, cr, cudaMemcpyDeviceToHost, I.down_stream, 4);
+        I.last_down += cr.width * cr.height * 4;
+        if (c_stage) {
+            downs.push_back(Down{cr, event(), nullptr});
+            ck(cudaEventRecord(downs.back().ev, I.down_stream), "cudaEventRecord");
+        }
+    }
+
+    // staged C: copy each region out as it lands (host pool; the caller helps)
+    void finish() {
+        if (!c_stage) return;
+        for (auto& d : downs) {
+            ck(cudaEventSynchronize(d.ev), "cudaEventSynchronize");
+            auto job = std::make_unique<rt::SnapJob>();
+            job->src = c_stage + d.r.off;
+            job->dst = C + d.r.off;
+            job->width = d.r.width;
+            job->height = d.r.height;
+            job->spitch = job->dpitch = d.r.pitch;
+            job->elem = 0;
+            if (d.r.width == d.r.pitch) {
+                job->width = d.r.width * d.r.height;
+                job->height = 1;
+            }
+            d.job = std::move(job);
+            pool->submit(d.job.get());
+        }
+        for (auto& d : downs) pool->wait(d.job.get());
+    }
+
+    void trace_pieces(const std::function<float(cudaEvent_t)>& at, const cudaEvent_t* ev_up) const {
+        std::fprintf(stderr, "%d pieces (%d host workers%s%s): up", static_cast<int>(pieces.size()),
+                     pool ? pool->workers() : -1, pinned[0] && pinned[1] ? "" : ", pageable input",
+                     c_stage ? ", pageable C" : "");
+        for (size_t j = 0; j < pieces.size(); ++j) {
+            const Piece& pc = pieces[j];
+            std::fprintf(stderr, " %c%d%s%.3f", pc.which ? 'B' : 'A', pc.tag, pc.job ? "h" : "", at(ev_up[j]));
+        }
+    }
+};
+
 double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, float* C, cudaStream_t s, int P,
                         int Q, char* base, const size_t* f32_in, const size_t* typed_in, size_t typed_c,
                         size_t f32_c) {
@@ -379,11 +642,9 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
         ck(cudaStreamCreateWithFlags(&I.up_stream, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&I.down_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     }
-    const BufferDecl& ra = I.root(0);
-    const BufferDecl& rb = I.root(1);
     const BufferDecl& rc = I.root(2);
-    const int ea = elem_code(ra.elem), eb = elem_code(rb.elem), ec = elem_code(rc.elem);
-    const size_t wa = byte_width(ra.elem), wb = byte_width(rb.elem), wc = byte_width(rc.elem);
+    const int ec = elem_code(rc.elem);
+    const size_t wa = byte_width(I.root(0).elem), wb = byte_width(I.root(1).elem), wc = byte_width(rc.elem);
     const long M = I.tp.M, N = I.tp.N, K = I.tp.K, lda = I.tp.lda, ldb = I.tp.ldb, ldc = I.tp.ldc;
     const bool a_row = !I.tc.a_mn_major, b_row = I.tc.b_mn_major != 0, c_row = I.tc.c_row_major != 0;
     const long mc = M / P, nc = N / Q;
@@ -391,14 +652,6 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
     auto b_region = [&](long c0, long c1) { return b_row ? Region{c0, c1 - c0, K, ldb} : Region{c0 * ldb, K, c1 - c0, ldb}; };
     auto c_region = [&](long r0, long r1, long c0, long c1) {
         return c_row ? Region{r0 * ldc + c0, c1 - c0, r1 - r0, ldc} : Region{r0 + c0 * ldc, r1 - r0, c1 - c0, ldc};
-    };
-    auto copy2d = [&](void* dst, const void* src, const Region& r, cudaMemcpyKind kind, cudaStream_t st,
-                      size_t w = 4) {
-        if (r.width == r.pitch)  // contiguous lines: one linear copy
-            ck(cudaMemcpyAsync(dst, src, static_cast<size_t>(r.width * r.height) * w, kind, st), "cudaMemcpyAsync");
-        else
-            ck(cudaMemcpy2DAsync(dst, r.pitch * w, src, r.pitch * w, r.width * w, r.height, kind, st),
-               "cudaMemcpy2DAsync");
     };
     // the panel order: A row panels and B column panels alternately, balanced by bytes
     const double a_piece = 4.0 * mc * K, b_piece = 4.0 * K * nc;
@@ -409,41 +662,15 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
         (take_a ? ia : ib)++;
     }
     const int np = P + Q;
-    // Each panel crosses PCIe as pieces of whole lines (~FI_HOST_PIECE_MB of
-    // fp32, default 8). Host snapping (runtime/host_snap.hpp): a fraction
-    // FI_HOST_SNAP_RATIO (default 0.8) of the pieces of f16/bf16 roots, spread
-    // evenly over the upload order, is converted by host cores into pinned
-    // staging while the copy engine moves the others as fp32 (snapped on the
-    // device), and then crosses in 2-byte elements. The ratio balances the two
-    // engines measured on the B200 box: the copy engine moves ~54 GB/s, the host
-    // converts ~60 GB/s of fp32 while the copy engine also reads host memory
-    // (profiles/round2/host_snap_probe.txt, host_snap_e2e_ab.log). The first FI_HOST_SNAP_SKIP pieces
-    // (default 1) are snapped on the device so the copy engine starts at once.
-    struct Piece {
-        int panel;
-        bool is_a;
-        Region r;
-        std::unique_ptr<rt::SnapJob> job;
-    };
-    std::vector<Piece> pieces;
+    HostIO io(I, s, base, f32_in, typed_in, A, B, C);
     std::vector<int> panel_end(static_cast<size_t>(np));  // one past each panel's last piece
-    {
-        double piece_bytes = 8.0 * (1 << 20);
-        if (const char* v = std::getenv("FI_HOST_PIECE_MB")) piece_bytes = std::atof(v) * (1 << 20);
-        for (int i = 0, ia = 0, ib = 0; i < np; ++i) {
-            const bool is_a = order[static_cast<size_t>(i)] == 'A';
-            const Region r = is_a ? a_region(ia * mc, (ia + 1) * mc) : b_region(ib * nc, (ib + 1) * nc);
-            (is_a ? ia : ib)++;
-            long nsub = std::lround(4.0 * r.width * r.height / piece_bytes);
-            nsub = std::max(1L, std::min(nsub, r.height));
-            for (long q = 0; q < nsub; ++q) {
-                const long l0 = r.height * q / nsub, l1 = r.height * (q + 1) / nsub;
-                pieces.push_back(Piece{i, is_a, Region{r.off + l0 * r.pitch, r.width, l1 - l0, r.pitch}, nullptr});
-            }
-            panel_end[static_cast<size_t>(i)] = static_cast<int>(pieces.size());
-        }
+    for (int i = 0, ia = 0, ib = 0; i < np; ++i) {
+        const bool is_a = order[static_cast<size_t>(i)] == 'A';
+        panel_end[static_cast<size_t>(i)] =
+            io.add(is_a ? 0 : 1, is_a ? a_region(ia * mc, (ia + 1) * mc) : b_region(ib * nc, (ib + 1) * nc), i);
+        (is_a ? ia : ib)++;
     }
-    const int npc = static_cast<int>(pieces.size());
+    const int npc = static_cast<int>(io.pieces.size());
     // events: [start][upload per piece][gemm begin, end per panel][C ready per panel][down done]
     const size_t need = 1 + npc + 2 * np + np + 1;
     while (I.pev.size() < need) {
@@ -453,91 +680,10 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
     }
     cudaEvent_t* ev = I.pev.data();
     cudaEvent_t ev_start = ev[0], *ev_up = ev + 1, *ev_g = ev_up + npc, *ev_c = ev_g + 2 * np, ev_down = ev_c[np];
-    rt::HostSnapPool* pool = (ea != 0 || eb != 0) ? rt::HostSnapPool::get() : nullptr;
-    if (pool) {
-        size_t hoff[2] = {0, 0}, hbytes = 0;
-        for (int w = 0; w < 2; ++w) {
-            hoff[w] = hbytes;
-            hbytes += (static_cast<size_t>(I.root(w).extent()) * 2 + 255) & ~size_t(255);
-        }
-        if (I.host_stage_bytes < hbytes) {
-            if (I.host_stage) cudaFreeHost(I.host_stage);
-            I.host_stage = nullptr;
-            I.host_stage_bytes = 0;
-            ck(cudaHostAlloc(&I.host_stage, hbytes, cudaHostAllocPortable), "cudaHostAlloc");
-            I.host_stage_bytes = hbytes;
-        }
-        int skip = 1;
-        if (const char* v = std::getenv("FI_HOST_SNAP_SKIP")) skip = std::atoi(v);
-        double ratio = 0.8;
-        if (const char* v = std::getenv("FI_HOST_SNAP_RATIO")) ratio = std::atof(v);
-        // fewer host threads convert proportionally less (16 measured)
-        ratio = std::min(ratio, ratio * (pool->workers() + 1) / 16.0);
-        for (int j = 0, h = 0; j < npc; ++j) {
-            Piece& pc = pieces[static_cast<size_t>(j)];
-            const int elem = pc.is_a ? ea : eb;
-            if (elem == 0 || j < skip) continue;
-            // piece j - skip is host-snapped when the running share crosses an integer
-            const int want = static_cast<int>(std::floor((j - skip + 1) * ratio + 1e-9));
-            if (want <= h) continue;
-            h = want;
-            auto job = std::make_unique<rt::SnapJob>();
-            job->src = (pc.is_a ? A : B) + pc.r.off;
-            job->dst = reinterpret_cast<uint16_t*>(static_cast<char*>(I.host_stage) + hoff[pc.is_a ? 0 : 1]) + pc.r.off;
-            job->width = pc.r.width;
-            job->height = pc.r.height;
-            job->spitch = job->dpitch = pc.r.pitch;
-            job->elem = elem;
-            if (pc.r.width == pc.r.pitch) {  // contiguous: one long line
-                job->width = pc.r.width * pc.r.height;
-                job->height = 1;
-            }
-            pc.job = std::move(job);
-        }
-        for (auto& pc : pieces)  // FIFO: converted in upload order
-            if (pc.job) pool->submit(pc.job.get());
-    }
-    // every submitted job is waited for, also when an upload below throws: the
-    // pool's workers must not touch a job (or the caller's A/B) after we return
-    struct JobGuard {
-        rt::HostSnapPool* pool;
-        std::vector<Piece>& pieces;
-        ~JobGuard() {
-            if (pool)
-                for (auto& pc : pieces)
-                    if (pc.job) pool->wait(pc.job.get());
-        }
-    } job_guard{pool, pieces};
+    io.start();
     ck(cudaEventRecord(ev_start, s), "cudaEventRecord");  // scratch reuse: after earlier work on s
     ck(cudaStreamWaitEvent(I.up_stream, ev_start, 0), "cudaStreamWaitEvent");
     ck(cudaStreamWaitEvent(I.down_stream, ev_start, 0), "cudaStreamWaitEvent");
-    // one piece: H2D into the fp32 staging (or straight into an fp32 root), then
-    // snapped to the root's element grid on s (sim.hpp:507-510); or, when host
-    // snapped, H2D of the snapped piece straight into the typed root
-    auto upload = [&](const Piece& pc, cudaEvent_t done) {
-        const int which = pc.is_a ? 0 : 1, elem = pc.is_a ? ea : eb;
-        const size_t w = pc.is_a ? wa : wb;
-        const Region& r = pc.r;
-        char* typed = base + typed_in[which];
-        if (pc.job) {
-            pool->wait(pc.job.get());
-            copy2d(typed + static_cast<size_t>(r.off) * w, reinterpret_cast<const char*>(pc.job->dst), r,
-                   cudaMemcpyHostToDevice, I.up_stream, w);
-            I.last_up += r.width * r.height * static_cast<long>(w);
-            ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
-            ck(cudaStreamWaitEvent(s, done, 0), "cudaStreamWaitEvent");
-            return;
-        }
-        const float* host = pc.is_a ? A : B;
-        float* stage = elem == 0 ? reinterpret_cast<float*>(typed) : reinterpret_cast<float*>(base + f32_in[which]);
-        copy2d(stage + r.off, host + r.off, r, cudaMemcpyHostToDevice, I.up_stream);
-        I.last_up += r.width * r.height * 4;
-        ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
-        ck(cudaStreamWaitEvent(s, done, 0), "cudaStreamWaitEvent");
-        if (elem != 0)
-            ck(rt::convert_f32_2d(stage + r.off, typed + static_cast<size_t>(r.off) * w, r.width, r.height, r.pitch, elem, s),
-               "input conversion");
-    };
     int ng = 0;
     auto gemm = [&](long r0, long r1, long c0, long c1) {
         sm100::TcGemmProblem p = I.tp;
@@ -560,13 +706,11 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
             result = reinterpret_cast<const float*>(base + f32_c);
         }
         ck(cudaEventRecord(ev_c[ng], s), "cudaEventRecord");
-        ck(cudaStreamWaitEvent(I.down_stream, ev_c[ng], 0), "cudaStreamWaitEvent");
-        copy2d(C + cr.off, result + cr.off, cr, cudaMemcpyDeviceToHost, I.down_stream);
-        I.last_down += cr.width * cr.height * 4;
+        io.download(result, cr, ev_c[ng]);
         ++ng;
     };
     for (int i = 0, ia = 0, ib = 0, j = 0; i < np; ++i) {
-        for (; j < panel_end[static_cast<size_t>(i)]; ++j) upload(pieces[static_cast<size_t>(j)], ev_up[j]);
+        for (; j < panel_end[static_cast<size_t>(i)]; ++j) io.upload(j, ev_up[j]);
         if (order[static_cast<size_t>(i)] == 'A') {
             ++ia;
             if (ib > 0) gemm((ia - 1) * mc, ia * mc, 0, ib * nc);
@@ -577,6 +721,7 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
     }
     ck(cudaEventRecord(ev_down, I.down_stream), "cudaEventRecord");
     ck(cudaStreamWaitEvent(s, ev_down, 0), "cudaStreamWaitEvent");
+    io.finish();
     ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     float ms_total = 0.f;
     for (int g = 0; g < ng; ++g) {
@@ -590,12 +735,8 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
             cudaEventElapsedTime(&ms, ev_start, e);
             return ms;
         };
-        std::fprintf(stderr, "blocked %dx%d panels, %d pieces (%d host workers): up", P, Q, npc,
-                     pool ? pool->workers() : -1);
-        for (int j = 0; j < npc; ++j) {
-            const Piece& pc = pieces[static_cast<size_t>(j)];
-            std::fprintf(stderr, " %c%d%s%.3f", pc.is_a ? 'A' : 'B', pc.panel, pc.job ? "h" : "", at(ev_up[j]));
-        }
+        std::fprintf(stderr, "blocked %dx%d panels, ", P, Q);
+        io.trace_pieces(at, ev_up);
         std::fprintf(stderr, " | gemm");
         for (int g = 0; g < ng; ++g) std::fprintf(stderr, " %.3f-%.3f", at(ev_g[2 * g]), at(ev_g[2 * g + 1]));
         std::fprintf(stderr, " | C down done %.3f\n", at(ev_down));
@@ -610,56 +751,44 @@ double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, f
         ck(cudaStreamCreateWithFlags(&I.up_stream, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&I.down_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     }
-    constexpr int kAPieces = 4;
-    // events: [start][A pieces][B panels][C panels][gemm begin/end per panel][down done]
-    const size_t need = 1 + kAPieces + 2 * chunks + 2 * chunks + 1;
+    const BufferDecl& ra = I.root(0);
+    const BufferDecl& rb = I.root(1);
+    const BufferDecl& rc = I.root(2);
+    const int ec = elem_code(rc.elem);
+    const size_t wb = byte_width(rb.elem), wc = byte_width(rc.elem);
+    HostIO io(I, s, base, f32_in, typed_in, A, B, C);
+    // A as one contiguous region (its storage), then B panel by panel
+    const long a_ext = ra.extent();
+    const int a_end = io.add(0, Region{0, a_ext, 1, a_ext}, 0);
+    const long nc = I.tp.N / chunks;  // columns per panel
+    const long b_ext = rb.extent(), c_ext = rc.extent();
+    std::vector<int> panel_end(static_cast<size_t>(chunks));
+    for (int j = 0; j < chunks; ++j) {
+        const long b0 = j * nc * I.tp.ldb, b1 = j + 1 == chunks ? b_ext : (j + 1) * nc * I.tp.ldb;
+        panel_end[static_cast<size_t>(j)] = io.add(1, Region{b0, b1 - b0, 1, b1 - b0}, j + 1);
+    }
+    const int npc = static_cast<int>(io.pieces.size());
+    // events: [start][upload per piece][C panels][gemm begin/end per panel][down done]
+    const size_t need = 1 + npc + chunks + 2 * chunks + 1;
     while (I.pev.size() < need) {
         cudaEvent_t e;
         ck(cudaEventCreate(&e), "cudaEventCreate");
         I.pev.push_back(e);
     }
     cudaEvent_t* ev = I.pev.data();
-    cudaEvent_t ev_start = ev[0], *ev_a = ev + 1, *ev_b = ev_a + kAPieces, *ev_c = ev_b + chunks;
+    cudaEvent_t ev_start = ev[0], *ev_up = ev + 1, *ev_c = ev_up + npc;
     cudaEvent_t *ev_g = ev_c + chunks, ev_down = ev_g[2 * chunks];
-    const BufferDecl& ra = I.root(0);
-    const BufferDecl& rb = I.root(1);
-    const BufferDecl& rc = I.root(2);
-    const int ea = elem_code(ra.elem), eb = elem_code(rb.elem), ec = elem_code(rc.elem);
-    const size_t wa = byte_width(ra.elem), wb = byte_width(rb.elem), wc = byte_width(rc.elem);
+    io.start();
     // scratch reuse across calls: the upload must not overtake earlier work on s
     ck(cudaEventRecord(ev_start, s), "cudaEventRecord");
     ck(cudaStreamWaitEvent(I.up_stream, ev_start, 0), "cudaStreamWaitEvent");
     ck(cudaStreamWaitEvent(I.down_stream, ev_start, 0), "cudaStreamWaitEvent");
-
-    // one storage range [e0, e1) of an input: H2D (into the f32 staging, or
-    // straight into the typed buffer for f32 roots), then snap on s
-    auto upload = [&](int which, const float* host, long e0, long e1, int elem, size_t w, cudaEvent_t done) {
-        if (e1 <= e0) {
-            ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
-            return;
-        }
-        char* typed = base + typed_in[which] + static_cast<size_t>(e0) * w;
-        float* stage = elem == 0 ? reinterpret_cast<float*>(typed)
-                                 : reinterpret_cast<float*>(base + f32_in[which]) + e0;
-        ck(cudaMemcpyAsync(stage, host + e0, static_cast<size_t>(e1 - e0) * 4, cudaMemcpyHostToDevice, I.up_stream),
-           "cudaMemcpyAsync");
-        I.last_up += (e1 - e0) * 4;
-        ck(cudaEventRecord(done, I.up_stream), "cudaEventRecord");
-        ck(cudaStreamWaitEvent(s, done, 0), "cudaStreamWaitEvent");
-        if (elem != 0)  // snapping to the root's element grid on ingestion (sim.hpp:507-510)
-            ck(rt::convert_f32(stage, typed, e1 - e0, elem, s), "input conversion");
-    };
-    const long a_ext = ra.extent();
-    for (int i = 0; i < kAPieces; ++i) {  // piece boundaries on 16-byte (4-element) multiples
-        const long e0 = (a_ext * i / kAPieces) & ~3L, e1 = i + 1 == kAPieces ? a_ext : (a_ext * (i + 1) / kAPieces) & ~3L;
-        upload(0, A, e0, e1, ea, wa, ev_a[i]);
-    }
-    const long nc = I.tp.N / chunks;  // columns per panel
-    const long b_ext = rb.extent(), c_ext = rc.extent();
+    int j_up = 0;
+    for (; j_up < a_end; ++j_up) io.upload(j_up, ev_up[j_up]);
     float ms_total = 0.f;
     for (int j = 0; j < chunks; ++j) {
-        const long b0 = j * nc * I.tp.ldb, b1 = j + 1 == chunks ? b_ext : (j + 1) * nc * I.tp.ldb;
-        upload(1, B, b0, b1, eb, wb, ev_b[j]);
+        for (; j_up < panel_end[static_cast<size_t>(j)]; ++j_up) io.upload(j_up, ev_up[j_up]);
+        const long b0 = j * nc * I.tp.ldb;
         sm100::TcGemmProblem p = I.tp;
         p.workspace = &I.ws;
         p.A = base + typed_in[0];
@@ -671,21 +800,19 @@ double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, f
         const int r = sm100::tc_gemm_launch(I.tc, p, s);
         check_tc_launch(r);
         ck(cudaEventRecord(ev_g[2 * j + 1], s), "cudaEventRecord");
-        const float* result = reinterpret_cast<const float*>(base + typed_c) + c0;
+        const float* result = reinterpret_cast<const float*>(base + typed_c);
         if (ec != 0) {
-            float* wide = reinterpret_cast<float*>(base + f32_c) + c0;
-            ck(rt::widen_to_f32(base + typed_c + static_cast<size_t>(c0) * wc, wide, c1 - c0, ec, s),
+            float* wide = reinterpret_cast<float*>(base + f32_c);
+            ck(rt::widen_to_f32(base + typed_c + static_cast<size_t>(c0) * wc, wide + c0, c1 - c0, ec, s),
                "output conversion");
             result = wide;
         }
         ck(cudaEventRecord(ev_c[j], s), "cudaEventRecord");
-        ck(cudaStreamWaitEvent(I.down_stream, ev_c[j], 0), "cudaStreamWaitEvent");
-        ck(cudaMemcpyAsync(C + c0, result, static_cast<size_t>(c1 - c0) * 4, cudaMemcpyDeviceToHost, I.down_stream),
-           "cudaMemcpyAsync");
-        I.last_down += (c1 - c0) * 4;
+        io.download(result, Region{c0, c1 - c0, 1, c1 - c0}, ev_c[j]);
     }
     ck(cudaEventRecord(ev_down, I.down_stream), "cudaEventRecord");
     ck(cudaStreamWaitEvent(s, ev_down, 0), "cudaStreamWaitEvent");
+    io.finish();
     ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     for (int j = 0; j < chunks; ++j) {
         float ms = 0.f;
@@ -698,10 +825,8 @@ double run_host_pipelined(const Plan::Impl& I, const float* A, const float* B, f
             cudaEventElapsedTime(&ms, ev_start, e);
             return ms;
         };
-        std::fprintf(stderr, "pipeline %d panels: A up", chunks);
-        for (int i = 0; i < kAPieces; ++i) std::fprintf(stderr, " %.3f", at(ev_a[i]));
-        std::fprintf(stderr, " | B up");
-        for (int j = 0; j < chunks; ++j) std::fprintf(stderr, " %.3f", at(ev_b[j]));
+        std::fprintf(stderr, "pipeline %d panels, ", chunks);
+        io.trace_pieces(at, ev_up);
         std::fprintf(stderr, " | gemm");
         for (int j = 0; j < chunks; ++j) std::fprintf(stderr, " %.3f-%.3f", at(ev_g[2 * j]), at(ev_g[2 * j + 1]));
         std::fprintf(stderr, " | C down done %.3f\n", at(ev_down));

@@ -115,7 +115,7 @@ __device__ __forceinline__ void epilogue_bar() { asm volatile("bar.sync 1, 128;"
 
 // Kernel body; the tensor maps must be __grid_constant__ kernel parameters
 // (TMA reads them through their parameter-space address).
-template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves, int kMcast, int kKB>
+template <int kCtaGroup, int BN, int kSplitK, int kSlabs, int kNHalves, int kMcast, int kKB = 1>
 __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB,
                                                    const CUtensorMap& tmB2, const CUtensorMap& tmC,
                                                    const CUtensorMap& tmC2,

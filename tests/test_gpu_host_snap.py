@@ -72,3 +72,38 @@ def test_run_host_host_snapped_panels_bit_identical(fi, oracle, monkeypatch, cap
     b = oracle.fill(k, n, 4, True)
     want = oracle.gemm_f64(oracle.round_elem(a, ab), oracle.round_elem(b, ab))
     assert np.array_equal(plan.run_host(a, b), want)
+
+
+@pytest.mark.parametrize("pin_in,pin_out", [(True, False), (False, True), (False, False), (True, True)])
+def test_run_host_pinned_and_pageable_buffers(fi, oracle, monkeypatch, capfd, pin_in, pin_out):
+    """anvil::Matrix holds std::vector storage (pageable); the benchmark uses
+    pinned buffers. Pageable inputs are snapped on the host entirely, a
+    pageable C is staged in pinned memory and copied out by the host pool;
+    every combination is exact against fp64 on integer inputs, in both
+    pipelines (blocked and column panels)."""
+    import torch
+    monkeypatch.setenv("FI_HOST_PIPELINE_TRACE", "1")
+    m, n, k = 1024, 2048, 1024
+    plan = fi.Plan(fi.strategies.tc_strategy(m, n, k, pair=True, tile_n=256))
+    a = oracle.fill(m, k, 3, True)
+    b = oracle.fill(k, n, 4, True)
+    want = oracle.gemm_f64(oracle.round_elem(a, "f16"), oracle.round_elem(b, "f16"))
+    # physical col-major storage of the roots
+    pa, pb = np.asfortranarray(a).ravel(order="K"), np.asfortranarray(b).ravel(order="K")
+    def buf(x, pinned):
+        t = torch.from_numpy(np.ascontiguousarray(x))
+        return t.pin_memory() if pinned else t
+    hA, hB = buf(pa, pin_in), buf(pb, pin_in)
+    hC = buf(np.zeros(m * n, np.float32), pin_out)
+    for mode in ["blocked", "panels"]:
+        monkeypatch.setenv("FI_HOST_PIPELINE", "1" if mode == "blocked" else "panels")
+        monkeypatch.setenv("FI_HOST_PANEL_MB", "1")
+        monkeypatch.setenv("FI_HOST_MIN_LINE", "128")
+        monkeypatch.setenv("FI_HOST_PIECE_MB", "1")
+        hC.zero_()
+        plan.run_host_ptr(hA.data_ptr(), hB.data_ptr(), hC.data_ptr())
+        trace = capfd.readouterr().err
+        assert ("pageable input" in trace) == (not pin_in), trace
+        assert ("pageable C" in trace) == (not pin_out), trace
+        c = hC.numpy().reshape(n, m).T  # col-major C
+        assert np.array_equal(c, want), mode
