@@ -21,10 +21,11 @@ def main(path):
                     cur.setdefault("drain", []).append((vals[10] - vals[4], vals[8] - vals[10]))
                 if len(vals) >= 13 and vals[12] and vals[11]:
                     cur.setdefault("drain_clk", []).append(vals[12] - vals[11])
-                if len(vals) >= 14 and vals[13] and vals[1] == 0:
-                    cur.setdefault("entry", []).append((vals[13], vals[2]))
-                if len(vals) >= 14 and vals[13] and vals[1] in (1, 2):
-                    cur.setdefault("pro%d" % vals[1], {})[vals[0]] = vals[13]
+            # prologue stamps (slot 7 of units 0..2): entry, TMEM alloc done, prologue synced
+            if len(vals) >= 14 and vals[13] and vals[1] == 0:
+                cur.setdefault("entry", []).append((vals[13], vals[2]))
+            if len(vals) >= 14 and vals[13] and vals[1] in (1, 2):
+                cur.setdefault("pro%d" % vals[1], {})[vals[0]] = vals[13]
             if len(vals) >= 8 and vals[6] and vals[7] and vals[3] > vals[2]:
                 cur.setdefault("mhz", []).append((vals[7] - vals[6]) / (vals[3] - vals[2]) * 1e3)
     last = launches[-1]
