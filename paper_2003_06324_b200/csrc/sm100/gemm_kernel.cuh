@@ -808,6 +808,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             have = have_next;
         }
         if (q == 0 && lane == 0) bulk_wait_group<0>();  // TMA stores of C complete
+        if (q == 0 && lane == 0 && args.trace) args.trace[(blockIdx.x * 16 + 3) * 16 + 7] = global_timer_ns();
         __syncwarp();
     }
 
@@ -816,6 +817,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<kCtaGroup>(tmem_base, S::TMEM_COLS);
+        if (lane == 0 && args.trace) args.trace[(blockIdx.x * 16 + 4) * 16 + 7] = global_timer_ns();
     }
 }
 

@@ -5,4 +5,4 @@ FI_TC_EPI_POLL1=$v timeout 600 ncu --metrics smsp__inst_executed.sum,gpc__cycles
 grep -E "inst_executed|per_second|gpu__time|elapsed.max" gpurun_out/ncu_8192_poll$v.log | sed "s/^/poll1=$v /"
 done
 VAR=FI_TC_EPI_POLL1 A=0 B=1 WL=c2 bash scripts/gpu_ab.sh
-for v in 0 1 0 1; do FI_TC_EPI_POLL1=$v timeout 300 python bench.py --workload c5 --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('c5 poll1=$v', round(d['value'],1), 'min', round(d['config']['ms_min'],3), 'med', round(d['config']['ms_median'],3), d['clocks'])"; done
+for v in 0 1 0 1; do FI_TC_EPI_POLL1=$v timeout 300 python bench.py --workload c5 --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('c5 poll1=$v', round(d['value'],1), 'min', round(d['impl_config']['ms_min'],3), 'med', round(d['impl_config']['ms_median'],3), d['clocks'])"; done

@@ -2,7 +2,7 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest -x -q -m gpu tests/test_gpu_remainder.py tests/test_gpu_tc.py > gpurun_out/pytest_iter.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_iter.log
 for i in 1 2; do for d in -1 12 16 20; do
-  FI_TC_PULL_D=$d timeout 300 python bench.py --workload c2 --steps 40 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('pull_d=$d', round(d['value'],1), 'TF min_ms', round(d['config']['ms_min']*1e3,1), 'med_ms', round(d['config']['ms_median']*1e3,1))"
+  FI_TC_PULL_D=$d timeout 300 python bench.py --workload c2 --steps 40 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('pull_d=$d', round(d['value'],1), 'TF min_ms', round(d['impl_config']['ms_min']*1e3,1), 'med_ms', round(d['impl_config']['ms_median']*1e3,1))"
 done; done
 cat > /tmp/tr.py <<'PY'
 import os, sys, torch

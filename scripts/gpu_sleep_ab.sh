@@ -8,4 +8,4 @@ done
 VAR=FI_TC_EPI_SLEEP A=0 B=256 WL=c2 bash scripts/gpu_ab.sh
 VAR=FI_TC_EPI_SLEEP A=0 B=1000 WL=c2 bash scripts/gpu_ab.sh
 VAR=FI_TC_EPI_SLEEP A=0 B=256 WL=c3 bash scripts/gpu_ab.sh
-for v in 0 256 0 256; do FI_TC_EPI_SLEEP=$v timeout 300 python bench.py --workload c5 --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('c5 sleep=$v', round(d['value'],1), 'min', round(d['config']['ms_min'],3), 'med', round(d['config']['ms_median'],3), d['clocks'])"; done
+for v in 0 256 0 256; do FI_TC_EPI_SLEEP=$v timeout 300 python bench.py --workload c5 --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('c5 sleep=$v', round(d['value'],1), 'min', round(d['impl_config']['ms_min'],3), 'med', round(d['impl_config']['ms_median'],3), d['clocks'])"; done

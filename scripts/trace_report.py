@@ -24,7 +24,7 @@ def main(path):
             # prologue stamps (slot 7 of units 0..2): entry, TMEM alloc done, prologue synced
             if len(vals) >= 14 and vals[13] and vals[1] == 0:
                 cur.setdefault("entry", []).append((vals[13], vals[2]))
-            if len(vals) >= 14 and vals[13] and vals[1] in (1, 2):
+            if len(vals) >= 14 and vals[13] and vals[1] in (1, 2, 3, 4):
                 cur.setdefault("pro%d" % vals[1], {})[vals[0]] = vals[13]
             if len(vals) >= 8 and vals[6] and vals[7] and vals[3] > vals[2]:
                 cur.setdefault("mhz", []).append((vals[7] - vals[6]) / (vals[3] - vals[2]) * 1e3)
@@ -43,7 +43,8 @@ def main(path):
               f"TMA load median {statistics.median(lag):.2f} us, max {max(lag):.2f}; first entry -> last stamp "
               f"{(end - e0) / 1e3:.1f} us")
         ent = {c: e for c, (e, _) in zip([r[0] for r in rows if r[1] == 0], last["entry"])}
-        for key, what in (("pro1", "TMEM alloc done"), ("pro2", "prologue cluster sync done")):
+        for key, what in (("pro1", "TMEM alloc done"), ("pro2", "prologue cluster sync done"),
+                          ("pro3", "C stores complete"), ("pro4", "TMEM dealloc done (exit)")):
             d = [(t - ent[c]) / 1e3 for c, t in last.get(key, {}).items() if c in ent]
             if d:
                 print(f"  entry -> {what}: median {statistics.median(d):.2f} us, max {max(d):.2f}")
