@@ -317,9 +317,9 @@ def ours_single(args, fi, torch):
                     "host_input_bytes_per_step": 4 * (m * k + k * n),
                     "ms_per_step": e2e_s * 1e3, "ms_mean": statistics.mean(e2e_t) * 1e3,
                     "steps": e2e_steps, "timing": "median of per-call wall times",
-                    "api": "fi_plan_run_host (pinned fp32 host buffers; ~80% of the input pieces snapped to "
-                           "f16 by host threads and uploaded as 2-byte elements, the rest uploaded fp32 and "
-                           "snapped on the device)"},
+                    "api": "fi_plan_run_host (pinned fp32 host buffers; input pieces snapped to f16 by host "
+                           "threads and uploaded as 2-byte elements, the first piece uploaded fp32 and snapped "
+                           "on the device)"},
             "gpu_launches": args.steps,
             "clocks": clocks.summary()}
     print(json.dumps(line), flush=True)

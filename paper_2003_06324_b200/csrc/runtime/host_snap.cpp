@@ -82,6 +82,47 @@ __attribute__((target("avx2"))) void snap_bf16_avx2(const float* s, uint16_t* d,
     for (; i < n; ++i) d[i] = snap1_bf16(s[i]);
 }
 
+// AVX-512 fast paths: convert 16 elements with one instruction and fall back
+// to the exact 8-wide path only when a lane needs the reference's saturation or
+// the canonical NaN (an f16 result with an all-ones exponent: inf / NaN).
+__attribute__((target("avx512f,avx512bw,avx512vl,f16c"))) void snap_f16_avx512(const float* s, uint16_t* d, long n) {
+    long i = 0;
+    for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 31); ++i) d[i] = snap1_f16(s[i]);
+    const __m256i expmask = _mm256_set1_epi16(0x7C00);
+    for (; i + 16 <= n; i += 16) {
+        __m256i h = _mm512_cvtps_ph(_mm512_loadu_ps(s + i), _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
+        if (_mm256_cmpeq_epi16_mask(_mm256_and_si256(h, expmask), expmask)) {  // rare: inf / NaN lanes
+            const __m128i lo = cvt8_f16(_mm256_loadu_ps(s + i)), hi = cvt8_f16(_mm256_loadu_ps(s + i + 8));
+            h = _mm256_set_m128i(hi, lo);
+        }
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i), h);
+    }
+    for (; i < n; ++i) d[i] = snap1_f16(s[i]);
+}
+
+__attribute__((target("avx512f,avx512bw,avx512vl"))) void snap_bf16_avx512(const float* s, uint16_t* d, long n) {
+    long i = 0;
+    for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 31); ++i) d[i] = snap1_bf16(s[i]);
+    const __m512i bias = _mm512_set1_epi32(0x7fff), one = _mm512_set1_epi32(1), qnan = _mm512_set1_epi32(0x7fff);
+    for (; i + 16 <= n; i += 16) {
+        const __m512 v = _mm512_loadu_ps(s + i);
+        const __m512i u = _mm512_castps_si512(v);
+        __m512i r = _mm512_srli_epi32(_mm512_add_epi32(u, _mm512_add_epi32(bias, _mm512_and_si512(_mm512_srli_epi32(u, 16), one))), 16);
+        r = _mm512_mask_mov_epi32(r, _mm512_cmp_ps_mask(v, v, _CMP_UNORD_Q), qnan);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i), _mm512_cvtepi32_epi16(r));
+    }
+    for (; i < n; ++i) d[i] = snap1_bf16(s[i]);
+}
+
+bool cpu_avx512() {
+    static const bool ok = [] {
+        __builtin_cpu_init();
+        return __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
+               __builtin_cpu_supports("avx512vl") && __builtin_cpu_supports("f16c");
+    }();
+    return ok;
+}
+
 bool cpu_ok() {
     static const bool ok = [] {
         __builtin_cpu_init();
@@ -130,8 +171,14 @@ void convert_piece(SnapJob* j, long p) {
 bool host_snap_supported() { return cpu_ok(); }
 
 void snap_f32(const float* src, uint16_t* dst, long n, int elem) {
-    if (elem == 1) snap_f16_avx2(src, dst, n);
-    else snap_bf16_avx2(src, dst, n);
+    static const bool wide = cpu_avx512() && !(std::getenv("FI_HOST_SNAP_AVX2"));
+    if (wide) {
+        if (elem == 1) snap_f16_avx512(src, dst, n);
+        else snap_bf16_avx512(src, dst, n);
+    } else {
+        if (elem == 1) snap_f16_avx2(src, dst, n);
+        else snap_bf16_avx2(src, dst, n);
+    }
 }
 
 HostSnapPool::HostSnapPool(int n) : nworkers_(n) {

@@ -381,13 +381,15 @@ bool blocked_split(const Plan::Impl& I, int& P, int& Q) {
 // ---------------------------------------------------------------- host side of both pipelines
 // Uploads: each input region is cut into pieces of whole lines (~FI_HOST_PIECE_MB
 // of fp32, default 8). Host snapping (runtime/host_snap.hpp): a fraction
-// FI_HOST_SNAP_RATIO (default 0.8) of the pieces of f16/bf16 roots, spread
+// FI_HOST_SNAP_RATIO (default 1: all but the first) of the pieces of f16/bf16 roots, spread
 // evenly over the upload order, is converted by host cores into pinned staging
 // while the copy engine moves the others as fp32 (snapped on the device), and
 // then crosses PCIe in 2-byte elements. The ratio balances the two engines
-// measured on the B200 box: the copy engine moves ~54 GB/s, the host converts
-// ~60 GB/s of fp32 while the copy engine also reads host memory
-// (profiles/round2/host_snap_probe.txt, host_snap_e2e_ab.log). The first
+// measured on the B200 box: the copy engine moves ~54 GB/s; with the AVX-512
+// conversion (112 GB/s alone on 16 threads) the host keeps ahead of the copy
+// engine even while it also reads host memory, so every piece but the first is
+// host-snapped (0.8 was best with the slower AVX2 conversion;
+// profiles/round2/host_snap_probe.txt, host_snap_e2e_ab.log, host_snap_avx512.log). The first
 // FI_HOST_SNAP_SKIP pieces (default 1) are snapped on the device so the copy
 // engine starts at once. Pageable inputs (anvil::Matrix is a std::vector) are
 // snapped on the host entirely: the driver's staged pageable copies are slower
@@ -519,7 +521,7 @@ struct HostIO {
         // starts at once), none for pageable ones (their staged copies are slow)
         int skip = -1;
         if (const char* v = std::getenv("FI_HOST_SNAP_SKIP")) skip = std::atoi(v);
-        double ratio = 0.8;
+        double ratio = 1.0;
         if (const char* v = std::getenv("FI_HOST_SNAP_RATIO")) ratio = std::atof(v);
         ratio = std::min(ratio, ratio * (pool->workers() + 1) / 16.0);  // fewer host threads convert less
         const int npc = static_cast<int>(pieces.size());

@@ -61,3 +61,22 @@ def test_grid_values_round_trip(fi, oracle):
     r = oracle.round_elem(a, "f16")
     np.testing.assert_array_equal(fi.host_snap(r, "f16").view(np.float16).astype(np.float32), r)
     np.testing.assert_array_equal(fi.host_snap(a, "f16").view(np.float16).astype(np.float32), r)
+
+
+def test_avx2_path_in_a_subprocess(fi):
+    """The AVX-512 fast path is the default where the CPU has it; the AVX2 path
+    (FI_HOST_SNAP_AVX2=1, read once per process) must agree bit for bit."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
+            "import numpy as np, paper_2003_06324_b200 as fi, test_host_snap as t;"
+            "rng = np.random.default_rng(5);"
+            "x = np.concatenate([t.SPECIALS, -t.SPECIALS, t.payload_nans(),"
+            " rng.integers(0, 2**32, size=100003, dtype=np.uint64).astype(np.uint32).view(np.float32)]);"
+            "assert (fi.host_snap(x, 'f16') == t.ref_f16(x)).all();"
+            "assert (fi.host_snap(x, 'bf16') == t.ref_bf16(x)).all(); print('ok')")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**os.environ, "FI_HOST_SNAP_AVX2": "1"}, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr
