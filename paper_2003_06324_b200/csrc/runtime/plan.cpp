@@ -502,21 +502,12 @@ struct HostIO {
         return static_cast<int>(pieces.size());
     }
 
-    // decide host / device snapping per piece and start the host conversions
+    // decide host / device snapping per piece and start the host conversions.
+    // Host-snapped pieces are staged densely packed, so their upload reads host
+    // memory sequentially even when the piece is a pitched panel of the root
+    // (short lines cost PCIe bandwidth, profiles/round1/e2e_host_pipeline.txt).
     void start() {
         if (!pool || (elem[0] == 0 && elem[1] == 0)) return;
-        size_t hoff[2] = {0, 0}, hbytes = 0;
-        for (int i = 0; i < 2; ++i) {
-            hoff[i] = hbytes;
-            hbytes += (static_cast<size_t>(I.root(i).extent()) * 2 + 255) & ~size_t(255);
-        }
-        if (I.host_stage_bytes < hbytes) {
-            if (I.host_stage) cudaFreeHost(I.host_stage);
-            I.host_stage = nullptr;
-            I.host_stage_bytes = 0;
-            ck(cudaHostAlloc(&I.host_stage, hbytes, cudaHostAllocPortable), "cudaHostAlloc");
-            I.host_stage_bytes = hbytes;
-        }
         // leading pieces snapped on the device: 1 for pinned inputs (the copy engine
         // starts at once), none for pageable ones (their staged copies are slow)
         int skip = -1;
@@ -525,27 +516,45 @@ struct HostIO {
         if (const char* v = std::getenv("FI_HOST_SNAP_RATIO")) ratio = std::atof(v);
         ratio = std::min(ratio, ratio * (pool->workers() + 1) / 16.0);  // fewer host threads convert less
         const int npc = static_cast<int>(pieces.size());
+        std::vector<size_t> off(static_cast<size_t>(npc), 0);
+        size_t hbytes = 0;
+        std::vector<char> host(static_cast<size_t>(npc), 0);
         for (int j = 0, h = 0; j < npc; ++j) {
-            Piece& pc = pieces[static_cast<size_t>(j)];
-            const int e = elem[pc.which];
-            if (e == 0) continue;
+            const Piece& pc = pieces[static_cast<size_t>(j)];
+            if (elem[pc.which] == 0) continue;
             const int sk = skip >= 0 ? skip : pinned[pc.which] ? 1 : 0;
             if (j < sk) continue;
-            bool host = !pinned[pc.which];  // pageable input: every piece
-            if (!host) {
-                // piece j - skip goes to the host when the running share crosses an integer
-                const int want = static_cast<int>(std::floor((j - skip + 1) * ratio + 1e-9));
-                host = want > h;
+            bool on_host = !pinned[pc.which];  // pageable input: every piece
+            if (!on_host) {
+                // piece j - sk goes to the host when the running share crosses an integer
+                const int want = static_cast<int>(std::floor((j - sk + 1) * ratio + 1e-9));
+                on_host = want > h;
                 h = std::max(h, want);
             }
-            if (!host) continue;
+            if (!on_host) continue;
+            host[static_cast<size_t>(j)] = 1;
+            off[static_cast<size_t>(j)] = hbytes;
+            hbytes += (static_cast<size_t>(pc.r.width * pc.r.height) * 2 + 255) & ~size_t(255);
+        }
+        if (hbytes == 0) return;
+        if (I.host_stage_bytes < hbytes) {
+            if (I.host_stage) cudaFreeHost(I.host_stage);
+            I.host_stage = nullptr;
+            I.host_stage_bytes = 0;
+            ck(cudaHostAlloc(&I.host_stage, hbytes, cudaHostAllocPortable), "cudaHostAlloc");
+            I.host_stage_bytes = hbytes;
+        }
+        for (int j = 0; j < npc; ++j) {
+            if (!host[static_cast<size_t>(j)]) continue;
+            Piece& pc = pieces[static_cast<size_t>(j)];
             auto job = std::make_unique<rt::SnapJob>();
             job->src = in[pc.which] + pc.r.off;
-            job->dst = reinterpret_cast<uint16_t*>(static_cast<char*>(I.host_stage) + hoff[pc.which]) + pc.r.off;
+            job->dst = static_cast<char*>(I.host_stage) + off[static_cast<size_t>(j)];
             job->width = pc.r.width;
             job->height = pc.r.height;
-            job->spitch = job->dpitch = pc.r.pitch;
-            job->elem = e;
+            job->spitch = pc.r.pitch;
+            job->dpitch = pc.r.width;  // packed
+            job->elem = elem[pc.which];
             if (pc.r.width == pc.r.pitch) {  // contiguous: one long line
                 job->width = pc.r.width * pc.r.height;
                 job->height = 1;
@@ -575,8 +584,14 @@ struct HostIO {
         char* typed = base + typed_in[which];
         if (pc.job) {
             pool->wait(pc.job.get());
-            copy2d(typed + static_cast<size_t>(r.off) * w[which], pc.job->dst, r, cudaMemcpyHostToDevice, I.up_stream,
-                   w[which]);
+            if (r.width == r.pitch)
+                ck(cudaMemcpyAsync(typed + static_cast<size_t>(r.off) * w[which], pc.job->dst,
+                                   static_cast<size_t>(r.width * r.height) * w[which], cudaMemcpyHostToDevice, I.up_stream),
+                   "cudaMemcpyAsync");
+            else  // packed staging -> pitched root
+                ck(cudaMemcpy2DAsync(typed + static_cast<size_t>(r.off) * w[which], r.pitch * w[which], pc.job->dst,
+                                     r.width * w[which], r.width * w[which], r.height, cudaMemcpyHostToDevice, I.up_stream),
+                   "cudaMemcpy2DAsync");
             I.last_up += r.width * r.height * static_cast<long>(w[which]);
         } else {
             float* stage = e == 0 ? reinterpret_cast<float*>(typed) : reinterpret_cast<float*>(base + f32_in[which]);
