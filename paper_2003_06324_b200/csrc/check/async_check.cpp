@@ -147,6 +147,7 @@ public:
             for (auto* b : {&c.tfull[0], &c.tfull[1], &c.tempty[0], &c.tempty[1], &c.rfull, &c.rempty, &c.stage,
                             &c.pstage[0], &c.pstage[1]})
                 init_bar(*b, 1);
+            for (auto& b : c.src) init_bar(b, 1);
             for (auto& b : c.full) init_bar(b, 1);
             for (auto& b : c.empty)  // a release from every pair reading the slot
                 init_bar(b, opt_.mutation == kMutMcastSingleRelease ? 1 : kMcast);
@@ -220,7 +221,7 @@ public:
 private:
     struct Cta {
         std::vector<Barrier> full, empty;
-        Barrier tfull[2], tempty[2], rfull, rempty, stage, pstage[2];
+        Barrier tfull[2], tempty[2], rfull, rempty, stage, pstage[2], src[8];
         std::deque<std::pair<Clock, Clock>> groups;  // committed bulk groups: (read clock, write clock)
         long committed = 0, waited_r = 0, waited_w = 0;
     };
@@ -685,11 +686,9 @@ private:
                     f.clock = ve;  // st.release.gpu
                     if (opt_.mutation == kMutFlagBeforeBulkWait) wait_groups(cta, 0, true);
                     if (nown > 0) {
-                        Barrier& sb = C.stage;
-                        const long bytes = static_cast<long>(nsrc - 1) * nown * kChunkBytes;
-                        expect_tx(sb, bytes);
-                        tick();
-                        arrive(sb, ve);
+                        // every source's chunks of my range land on their own barrier
+                        // (the kernel issues them in arrival order; each copy follows
+                        // the acquire of its source's flag either way)
                         for (int j = 0; j < nsrc; ++j) {
                             if (j == s) continue;
                             const long ps = j < nslc ? tile_idx + static_cast<long>(j) * rest
@@ -703,6 +702,9 @@ private:
                             co_await WaitUntil{[&pf, this] { return pf.value >= a_.epoch; }};
                             join(ve, pf.clock);  // ld.acquire.gpu
                             tick();
+                            Barrier& sb = C.src[j];
+                            expect_tx(sb, static_cast<long>(nown) * kChunkBytes);
+                            arrive(sb, ve);
                             issue(G, E);
                             workspace(G, ps, c_lo, nown, false);
                             const int pj = opt_.mutation == kMutUnpackedPeerStaging ? j : (j < s ? j : j - 1);
@@ -710,25 +712,27 @@ private:
                                  static_cast<long>(nown) * kChunkBytes, true);
                             complete_tx(sb, static_cast<long>(nown) * kChunkBytes, vc_[static_cast<size_t>(G)]);
                         }
-                        co_await wait(sb, 0);
-                        acquire(E, sb, 0);
+                        // sum in slice order as the sources land; a TMA C stores each
+                        // chunk as soon as it is summed
                         for (int c = c_lo; c < c_hi; ++c) {
                             for (int j = 0; j < nsrc; ++j) {
+                                if (j != s && c == c_lo) {
+                                    co_await wait(C.src[j], 0);
+                                    acquire(E, C.src[j], 0);
+                                }
                                 const int pj = opt_.mutation == kMutUnpackedPeerStaging ? j : (j < s ? j : j - 1);
                                 const long off = j == s ? static_cast<long>(c - c_lo) * kChunkBytes
                                                         : peer0 + (static_cast<long>(pj) * nown + (c - c_lo)) * kChunkBytes;
                                 smem(E, cta, kRing, off, kChunkBytes, false);
                             }
-                            if (a_.c_tma)
+                            if (a_.c_tma) {
                                 smem(E, cta, kRing, static_cast<long>(c - c_lo) * kChunkBytes, kChunkBytes, true);
-                            else
-                                store_c(E, tile, c);
-                        }
-                        if (a_.c_tma) {
-                            for (int c = c_lo; c < c_hi; ++c)
                                 bulk_store(kRing, static_cast<long>(c - c_lo) * kChunkBytes,
                                            [&](int bw) { store_c(bw, tile, c); });
-                            commit_group(cta);
+                                commit_group(cta);
+                            } else {
+                                store_c(E, tile, c);
+                            }
                         }
                     }
                 }

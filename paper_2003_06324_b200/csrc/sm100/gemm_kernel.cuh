@@ -150,6 +150,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     uint64_t* rempty_bar = bars + 2 * kStages + 5;  // split-K: all peers done reading
     uint64_t* stage_bar = bars + 2 * kStages + 6;   // [2] stream-K fixup staging
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 8);
+    uint64_t* src_bar = bars + 2 * kStages + 10;    // [8] symmetric fixup: one per K-slice source
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -179,6 +180,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         mbar_init(rempty_bar, 4 * kSplitK);
         mbar_init(&stage_bar[0], 1);
         mbar_init(&stage_bar[1], 1);
+        for (int j = 0; j < 8; ++j) mbar_init(&src_bar[j], 1);
         fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
@@ -688,31 +690,39 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                         trace_stamp(args, it - 1, 4);
                         st_release_gpu(args.flags + (u.slot * kCtaGroup + pair_rank), epoch);
                         if (nown > 0) {
-                            mbar_arrive_expect_tx(&stage_bar[0], (nsrc - 1) * nown * kChunkBytes);
-                            for (int j = 0; j < nsrc; ++j) {
-                                if (j == s) continue;
-                                const int ps = j < nslc ? tile_idx + j * rest  // slot of source j
-                                                        : remainder_slot(args, rest, nclusters, tile_idx);
-                                while (ld_acquire_gpu(args.flags + (ps * kCtaGroup + pair_rank)) < epoch)
-                                    __nanosleep(32);
-                                fence_proxy_async_global();
-                                bulk_copy_g2s(peer + (j < s ? j : j - 1) * nown * kChunkFloats,
-                                              args.workspace +
-                                                  static_cast<long>(ps * kCtaGroup + pair_rank) * S::WS_FLOATS +
-                                                  static_cast<long>(c_lo) * kChunkFloats,
-                                              nown * kChunkBytes, &stage_bar[0]);
+                            // fetch each source's chunks of my range as soon as its flag is
+                            // set (arrival order), each completing on its own barrier
+                            uint32_t pending = ((1u << nsrc) - 1u) & ~(1u << s);
+                            while (pending) {
+                                for (uint32_t rest_mask = pending; rest_mask; rest_mask &= rest_mask - 1) {
+                                    const int j = __ffs(rest_mask) - 1;
+                                    const int ps = j < nslc ? tile_idx + j * rest  // slot of source j
+                                                            : remainder_slot(args, rest, nclusters, tile_idx);
+                                    if (ld_acquire_gpu(args.flags + (ps * kCtaGroup + pair_rank)) < epoch) continue;
+                                    fence_proxy_async_global();
+                                    mbar_arrive_expect_tx(&src_bar[j], nown * kChunkBytes);
+                                    bulk_copy_g2s(peer + (j < s ? j : j - 1) * nown * kChunkFloats,
+                                                  args.workspace +
+                                                      static_cast<long>(ps * kCtaGroup + pair_rank) * S::WS_FLOATS +
+                                                      static_cast<long>(c_lo) * kChunkFloats,
+                                                  nown * kChunkBytes, &src_bar[j]);
+                                    pending &= ~(1u << j);
+                                }
+                                if (pending) __nanosleep(32);
                             }
                         }
                     }
                     __syncwarp();
                     if (nown > 0) {
-                        mbar_wait(&stage_bar[0], 0);
-                        if (q == 0 && lane == 0) trace_stamp(args, it - 1, 5);
+                        // sum in slice order (deterministic) as the sources land; with a TMA
+                        // C the chunk is stored as soon as it is summed
+                        const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
 #pragma unroll 1
                         for (int c = c_lo; c < c_hi; ++c) {
                             float v[32];
 #pragma unroll 1
                             for (int j = 0; j < nsrc; ++j) {
+                                if (j != s && c == c_lo) mbar_wait(&src_bar[j], 0);
                                 const float* src = (j == s ? own : peer + (j < s ? j : j - 1) * nown * kChunkFloats) +
                                                    (c - c_lo) * kChunkFloats + row;
                                 if (j == 0) {
@@ -723,22 +733,19 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                                     for (int x = 0; x < 32; ++x) v[x] += src[x * S::BM];
                                 }
                             }
-                            if (args.c_tma) {  // sum in place; TMA-stored below
+                            if (c == c_lo && q == 0 && lane == 0) trace_stamp(args, it - 1, 5);
+                            if (args.c_tma) {  // sum in place, TMA-store the chunk
                                 float* dst = own + (c - c_lo) * kChunkFloats + row;
 #pragma unroll
                                 for (int x = 0; x < 32; ++x) dst[x * S::BM] = v[x];
+                                fence_proxy_async();
+                                epilogue_bar();
+                                if (q == 0 && lane == 0) {
+                                    tma_store_2d(&tmC, own + (c - c_lo) * kChunkFloats, m_cta, tn * BN + c * 32);
+                                    bulk_commit_group();
+                                }
                             } else {
                                 store_row32_any(args, m, tn * BN + c * 32, v);
-                            }
-                        }
-                        if (args.c_tma) {
-                            fence_proxy_async();
-                            epilogue_bar();
-                            if (q == 0 && lane == 0) {
-                                const int m_cta = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
-                                for (int c = c_lo; c < c_hi; ++c)
-                                    tma_store_2d(&tmC, own + (c - c_lo) * kChunkFloats, m_cta, tn * BN + c * 32);
-                                bulk_commit_group();
                             }
                         }
                     }
