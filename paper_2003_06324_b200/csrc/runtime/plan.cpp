@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <fstream>
 #include <functional>
 #include <algorithm>
@@ -463,6 +464,13 @@ struct HostIO {
     // every submitted job is waited for, also when an enqueue throws: the pool's
     // workers must not touch a job (or the caller's buffers) after we return
     ~HostIO() {
+        // an enqueue failed mid-call: copies already queued may still read the
+        // pinned staging (or write C) -- drain them before the staging is reused
+        if (std::uncaught_exceptions() > 0) {
+            if (I.up_stream) cudaStreamSynchronize(I.up_stream);
+            if (I.down_stream) cudaStreamSynchronize(I.down_stream);
+            cudaGetLastError();
+        }
         if (!pool) return;
         for (auto& p : pieces)
             if (p.job) pool->wait(p.job.get());
