@@ -11,6 +11,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -663,6 +664,7 @@ struct HostIO {
 double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, float* C, cudaStream_t s, int P,
                         int Q, char* base, const size_t* f32_in, const size_t* typed_in, size_t typed_c,
                         size_t f32_c) {
+    const auto h_setup = std::chrono::steady_clock::now();
     if (!I.up_stream) {
         ck(cudaStreamCreateWithFlags(&I.up_stream, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamCreateWithFlags(&I.down_stream, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -709,6 +711,7 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
     ck(cudaEventRecord(ev_start, s), "cudaEventRecord");  // scratch reuse: after earlier work on s
     ck(cudaStreamWaitEvent(I.up_stream, ev_start, 0), "cudaStreamWaitEvent");
     ck(cudaStreamWaitEvent(I.down_stream, ev_start, 0), "cudaStreamWaitEvent");
+    const auto h_start = std::chrono::steady_clock::now();
     int ng = 0;
     auto gemm = [&](long r0, long r1, long c0, long c1) {
         sm100::TcGemmProblem p = I.tp;
@@ -744,10 +747,12 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
             if (ia > 0) gemm(0, ia * mc, (ib - 1) * nc, ib * nc);
         }
     }
+    const auto h_enqueued = std::chrono::steady_clock::now();
     ck(cudaEventRecord(ev_down, I.down_stream), "cudaEventRecord");
     ck(cudaStreamWaitEvent(s, ev_down, 0), "cudaStreamWaitEvent");
     io.finish();
     ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    const auto h_done = std::chrono::steady_clock::now();
     float ms_total = 0.f;
     for (int g = 0; g < ng; ++g) {
         float ms = 0.f;
@@ -760,6 +765,11 @@ double run_host_blocked(const Plan::Impl& I, const float* A, const float* B, flo
             cudaEventElapsedTime(&ms, ev_start, e);
             return ms;
         };
+        auto us = [&](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+            return std::chrono::duration<double, std::micro>(b - a).count();
+        };
+        std::fprintf(stderr, "host: setup %.0f us, start->enqueued %.0f us, start->synced %.0f us | ",
+                     us(h_setup, h_start), us(h_start, h_enqueued), us(h_start, h_done));
         std::fprintf(stderr, "blocked %dx%d panels, ", P, Q);
         io.trace_pieces(at, ev_up);
         std::fprintf(stderr, " | gemm");
