@@ -278,7 +278,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                             } else if (args.a_mn_major) {
                                 // one 3D box {64, 64, 2}: both 64-row SW128 panels of the slab
                                 // (tmA viewed as 64 rows x K x M/64 panels) -- one TMA op instead
-                                // of two; the SM's TMA unit is a bottleneck of the main loop
+                                // of two (measured +3 % on C2)
                                 load3(sas, &tmA, 0, k0, m0s / 64);
                             } else {
                                 load(sas, &tmA, k0, m0s, pol_a);
