@@ -73,5 +73,11 @@ int main(int argc, char** argv) {
         for (long j = 0; j < 64; ++j) err = std::fmax(err, std::fabs(r.output.at(i, j) - want.at(i, j)));
     std::printf("gpu run: max_abs_error=%g digest=0x%016llx device_ms=%.4f\n", err,
                 static_cast<unsigned long long>(digest(r.output)), r.device_ms);
-    return err == 0 ? 0 : 2;
+    // the same call under the GPU-explicit names: bit-identical
+    GpuRunOptions go;
+    go.device = 0;
+    RunResult r2 = run_gpu(root, tree, a, &b, go);
+    const bool same = digest(r2.output) == digest(r.output);
+    std::printf("run_gpu: %s\n", same ? "identical" : "DIFFERENT");
+    return err == 0 && same ? 0 : 2;
 }

@@ -151,8 +151,23 @@ private:
 };
 
 // --- the execution seam ----------------------------------------------------
+// anvil::run (proj/include/anvil/sim.hpp:495 / :536) with the same signatures
+// and semantics (C = A*B from a zero C, F16 roots snapped on ingestion, output
+// in C's root layout), executed on the B200 instead of the CPU model.
 RunResult run(const Program& prog, const Matrix& a, const Matrix* b = nullptr, RunOptions opts = {});
 RunResult run(const Spec& root, const NodePtr& tree, const Matrix& a, const Matrix* b = nullptr,
               RunOptions opts = {}, const MicroKernelSet& mks = MicroKernelSet{});
+
+// The names SURVEY.md 8(b) gives the GPU entry points: run_gpu is run (which
+// already executes on the GPU); GpuRunOptions carries the device, the stream
+// and -- through RunResult::device_ms -- the kernel timing.
+using GpuRunOptions = RunOptions;
+inline RunResult run_gpu(const Program& prog, const Matrix& a, const Matrix* b = nullptr, GpuRunOptions opts = {}) {
+    return run(prog, a, b, opts);
+}
+inline RunResult run_gpu(const Spec& root, const NodePtr& tree, const Matrix& a, const Matrix* b = nullptr,
+                         GpuRunOptions opts = {}, const MicroKernelSet& mks = MicroKernelSet{}) {
+    return run(root, tree, a, b, opts, mks);
+}
 
 }  // namespace fireiron

@@ -40,3 +40,4 @@ def test_cpp_dropin_run_on_gpu(tmp_path):
     r = subprocess.run([str(exe), "gpu"], capture_output=True, text=True, env=env, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "max_abs_error=0 " in r.stdout
+    assert "run_gpu: identical" in r.stdout
