@@ -112,6 +112,7 @@ class ClockSampler:
 
     def __init__(self, device_index=0, period=0.001):
         self.samples, self.reasons, self.period = [], set(), period
+        self.power_w = []
         self.max_mhz = None
         self._stop = threading.Event()
         try:
@@ -127,6 +128,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.power_w.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit:
@@ -149,8 +151,12 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.power_w:
+            out["power_w_median"] = statistics.median(self.power_w)
+            out["power_w_max"] = max(self.power_w)
+        return out
 
 
 # ------------------------------------------------------------------ CPU baseline (reference)
