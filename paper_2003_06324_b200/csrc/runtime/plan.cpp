@@ -435,6 +435,8 @@ struct HostIO {
             cudaGetLastError();
             return false;
         }
+        if (a.type == cudaMemoryTypeDevice)  // the host pipelines read and write host memory
+            throw BackendError(104, "run_host expects host buffers (got a device pointer; use fi_plan_launch)");
         return a.type == cudaMemoryTypeHost;
     }
 

@@ -107,3 +107,19 @@ def test_run_host_pinned_and_pageable_buffers(fi, oracle, monkeypatch, capfd, pi
         assert ("pageable C" in trace) == (not pin_out), trace
         c = hC.numpy().reshape(n, m).T  # col-major C
         assert np.array_equal(c, want), mode
+
+
+def test_run_host_rejects_device_pointers(fi, monkeypatch):
+    """The host pipelines read and write host memory: a device pointer is an
+    argument error (FI_ERR_ARGUMENT), not a crash."""
+    import torch
+    monkeypatch.setenv("FI_HOST_PANEL_MB", "1")
+    monkeypatch.setenv("FI_HOST_MIN_LINE", "128")
+    m, n, k = 1024, 2048, 1024
+    plan = fi.Plan(fi.strategies.tc_strategy(m, n, k, pair=True, tile_n=256))
+    hA = torch.zeros(m * k, dtype=torch.float32, pin_memory=True)
+    hB = torch.zeros(k * n, dtype=torch.float32, pin_memory=True)
+    dC = torch.zeros(m * n, dtype=torch.float32, device="cuda")
+    with pytest.raises(fi.FiError) as e:
+        plan.run_host_ptr(hA.data_ptr(), hB.data_ptr(), dC.data_ptr())
+    assert e.value.code == 104
