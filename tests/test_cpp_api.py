@@ -41,3 +41,30 @@ def test_cpp_dropin_run_on_gpu(tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
     assert "max_abs_error=0 " in r.stdout
     assert "run_gpu: identical" in r.stdout
+
+
+def build_c(tmp_path):
+    exe = tmp_path / "capi_run_host"
+    subprocess.run([shutil.which("gcc"), "-std=c11", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "capi_run_host.c"),
+                    "-L", os.path.join(ROOT, "paper_2003_06324_b200", "_lib"), "-lfireiron_b200",
+                    "-o", str(exe)], check=True, capture_output=True, text=True)
+    env = dict(os.environ, LD_LIBRARY_PATH=os.path.join(ROOT, "paper_2003_06324_b200", "_lib"))
+    return exe, env
+
+
+@pytest.mark.skipif(shutil.which("gcc") is None, reason="gcc absent")
+def test_c_abi_example_parses(tmp_path):
+    """A plain-C caller compiles against include/fireiron_b200.h alone."""
+    exe, env = build_c(tmp_path)
+    r = subprocess.run([str(exe), "--parse"], capture_output=True, text=True, env=env, timeout=60)
+    assert r.returncode == 0 and r.stdout.startswith("valid; grid 4x4"), r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(shutil.which("gcc") is None, reason="gcc absent")
+def test_c_abi_example_runs_exact(tmp_path):
+    exe, env = build_c(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, env=env, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "max_abs_error=0" in r.stdout
