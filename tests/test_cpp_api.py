@@ -43,6 +43,17 @@ def test_cpp_dropin_run_on_gpu(tmp_path):
     assert "run_gpu: identical" in r.stdout
 
 
+@pytest.mark.gpu
+@pytest.mark.skipif(GXX is None, reason="g++ absent")
+def test_cpp_dropin_tensor_core_run_pageable(tmp_path):
+    """anvil::run on std::vector-backed matrices with a tensor-core strategy
+    large enough for the pipelined host path: exact on integer inputs."""
+    exe, env = build(tmp_path)
+    r = subprocess.run([str(exe), "gpu-tc"], capture_output=True, text=True, env=env, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "max_abs_error=0 " in r.stdout
+
+
 def build_c(tmp_path):
     exe = tmp_path / "capi_run_host"
     subprocess.run([shutil.which("gcc"), "-std=c11", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
