@@ -9,7 +9,11 @@
 //   done                                   -> UMMA leaf (tcgen05.mma kind::f16)
 //
 // Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (leader CTA),
-// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM -> RF -> GL).
+// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM -> RF -> GL). The
+// producer and MMA warps run their loops with all 32 lanes so every operand is
+// warp-uniform (uniform registers); one elected lane issues each TMA / MMA /
+// commit (elect.sync inside the asm) -- no per-issue waterfall, measured 3-16 %
+// faster on narrow tiles (profiles/round2/ab_warp_issue.log).
 // Accumulators are double-buffered in TMEM so the epilogue of one work unit
 // overlaps the main loop of the next. With kCtaGroup == 2 a CTA pair (cluster
 // of 2) computes a 256xBN tile with tcgen05.mma.cta_group::2: each CTA stages
@@ -203,7 +207,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
-        if (lane == 0) {
+        // the whole warp runs the loop so every operand is warp-uniform (uniform
+        // registers, no per-issue waterfall); lane 0 issues
+        {
+            const bool issuer = lane == 0;
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
@@ -227,7 +234,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 }
                 if (args.b_ready)  // gated B: the tile's column chunk has landed
                     wait_b_chunk(args.b_ready + tn / args.b_chunk_tiles, args.b_epoch);
-                trace_stamp(args, it, 0);
+                if (issuer) trace_stamp(args, it, 0);
                 ++it;
                 const int m0 = tm * S::BM_TILE + static_cast<int>(pair_rank) * S::BM;
                 const int n0 = tn * kBNTile + static_cast<int>(mc_rank) * S::BN_TILE + u.n_off +
@@ -240,24 +247,26 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     // kKB = 2: the box covers two K blocks even when the unit has one
                     // left (the second is read but not multiplied; past K it is zero-
                     // filled); the transaction count is the full box either way
-                    if (mma_leader) mbar_arrive_expect_tx(&full_bar[s], tx);
+                    if (mma_leader) mbar_arrive_expect_tx_warp(&full_bar[s], tx);
                     auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol) {
                         if (args.l2_hint) {
+                            if (!issuer) return;
                             if constexpr (kCtaGroup == 1) tma_load_2d_hint(dst, map, &full_bar[s], c0, c1, pol);
                             else tma_load_2d_pair_hint(dst, map, &full_bar[s], c0, c1, pol);
                         } else {
-                            if constexpr (kCtaGroup == 1) tma_load_2d(dst, map, &full_bar[s], c0, c1);
-                            else tma_load_2d_pair(dst, map, &full_bar[s], c0, c1);
+                            if constexpr (kCtaGroup == 1) tma_load_2d_warp(dst, map, &full_bar[s], c0, c1);
+                            else tma_load_2d_pair_warp(dst, map, &full_bar[s], c0, c1);
                         }
                     };
                     auto load3 = [&](void* dst, const CUtensorMap* map, int c0, int c1, int c2) {
-                        if constexpr (kCtaGroup == 1) tma_load_3d(dst, map, &full_bar[s], c0, c1, c2);
-                        else tma_load_3d_pair(dst, map, &full_bar[s], c0, c1, c2);
+                        if constexpr (kCtaGroup == 1) tma_load_3d_warp(dst, map, &full_bar[s], c0, c1, c2);
+                        else tma_load_3d_pair_warp(dst, map, &full_bar[s], c0, c1, c2);
                     };
                     if constexpr (kMcast > 1) {
                         // my 64-row half of the A block, to me and my rank-twin in the other pair
                         const int h = static_cast<int>(mc_rank);
-                        if (args.a_mn_major)
+                        if (!issuer) {
+                        } else if (args.a_mn_major)
                             tma_load_2d_pair_mc(sa + h * 8192, &tmA, &full_bar[s], m0 + h * 64, k0, mc_a_mask);
                         else  // tmA box: 64 K x 64 rows for multicast plans
                             tma_load_2d_pair_mc(sa + h * 8192, &tmA, &full_bar[s], k0, m0 + h * 64, mc_a_mask);
@@ -270,7 +279,8 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                                 // one box for both K blocks: MN-major {64, 64, 2 panels, 2 K blocks},
                                 // K-major {64 k, 128 rows, 2 K blocks}
                                 if (args.a_mn_major) {
-                                    if constexpr (kCtaGroup == 1) tma_load_4d(sas, &tmA, &full_bar[s], 0, 0, m0s / 64, kb0 + kb);
+                                    if (!issuer) {
+                                    } else if constexpr (kCtaGroup == 1) tma_load_4d(sas, &tmA, &full_bar[s], 0, 0, m0s / 64, kb0 + kb);
                                     else tma_load_4d_pair(sas, &tmA, &full_bar[s], 0, 0, m0s / 64, kb0 + kb);
                                 } else {
                                     load3(sas, &tmA, 0, m0s, kb0 + kb);
@@ -305,7 +315,9 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (mma_leader && lane == 0) {
+        if (mma_leader) {
+            const bool issuer = lane == 0;
+            const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);  // provably warp-uniform
             // instruction descriptor: f32 accumulate, a/b format, majors, N>>3, M>>4
             const uint32_t idesc_base = (1u << 4) | (static_cast<uint32_t>(args.ab_format) << 7) |
                                         (static_cast<uint32_t>(args.ab_format) << 10) |
@@ -329,7 +341,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 const uint32_t idesc = idesc_base | (static_cast<uint32_t>(u.width >> 3) << 17);
                 mbar_wait_cluster(&tempty_bar[buf], (use & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * S::ACC_COLS);
+                const uint32_t d_tmem = tmem_u + static_cast<uint32_t>(buf * S::ACC_COLS);
                 const uint32_t b_kb_bytes = static_cast<uint32_t>(u.width / kCtaGroup) * 128;  // B rows x 128 B
                 for (int kb = u.k0; kb < u.k1; kb += kKB) {
                     mbar_wait(&full_bar[s], ph);
@@ -349,26 +361,28 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                                 uint64_t bd0 = smem_desc_sw128(sb + b * b_kb_bytes + k * b_kstep, b_lbo, 1024);
                                 uint64_t bd1 = smem_desc_sw128(sb + kKB * S::HALF_B_BYTES + b * b_kb_bytes + k * b_kstep,
                                                                b_lbo, 1024);
-                                umma_f16_collect<kCtaGroup, 1>(d_tmem, ad, bd0, idesc, acc);
-                                umma_f16_collect<kCtaGroup, 2>(d_tmem + BN, ad, bd1, idesc, acc);
+                                umma_f16_collect_warp<kCtaGroup, 1>(d_tmem, ad, bd0, idesc, acc);
+                                umma_f16_collect_warp<kCtaGroup, 2>(d_tmem + BN, ad, bd1, idesc, acc);
                             } else {
                                 uint64_t bd = smem_desc_sw128(sb + b * b_kb_bytes + k * b_kstep, b_lbo, 1024);
 #pragma unroll
                                 for (int sl = 0; sl < kSlabs; ++sl) {  // slabs share the B operand
                                     uint64_t ad = smem_desc_sw128(
                                         sa + (sl * kKB + b) * S::SLAB_BYTES + k * a_kstep, a_lbo, 1024);
-                                    umma_f16<kCtaGroup>(d_tmem + sl * BN, ad, bd, idesc, acc);
+                                    umma_f16_warp<kCtaGroup>(d_tmem + sl * BN, ad, bd, idesc, acc);
                                 }
                             }
                         }
                     }
-                    if constexpr (kCtaGroup == 1) umma_commit(&empty_bar[s]);
-                    else umma_commit_pair(&empty_bar[s], kMcast > 1 ? mc_all : pair_mask);
+                    if constexpr (kCtaGroup == 1) umma_commit_warp(&empty_bar[s]);
+                    else umma_commit_pair_warp(&empty_bar[s], kMcast > 1 ? mc_all : pair_mask);
                     if (++s == nst) { s = 0; ph ^= 1; }
                 }
-                if constexpr (kCtaGroup == 1) umma_commit(&tfull_bar[buf]);
-                else umma_commit_pair(&tfull_bar[buf], pair_mask);
-                trace_stamp(args, it - 1, 1);
+                if (issuer) {
+                    if constexpr (kCtaGroup == 1) umma_commit(&tfull_bar[buf]);
+                    else umma_commit_pair(&tfull_bar[buf], pair_mask);
+                    trace_stamp(args, it - 1, 1);
+                }
             }
         }
     } else if (warp >= 4) {
