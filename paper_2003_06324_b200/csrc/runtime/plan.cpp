@@ -428,6 +428,8 @@ struct HostIO {
     std::vector<Piece> pieces;
     std::vector<Down> downs;
     size_t nev = 0;
+    const bool tracing = std::getenv("FI_HOST_PIPELINE_TRACE") != nullptr;
+    std::vector<std::pair<long, cudaEvent_t>> down_done;  // traced: bytes and completion of each C region
 
     static bool is_pinned(const void* p) {
         cudaPointerAttributes a;
@@ -474,6 +476,7 @@ struct HostIO {
             if (I.down_stream) cudaStreamSynchronize(I.down_stream);
             cudaGetLastError();
         }
+        for (auto& d : down_done) cudaEventDestroy(d.second);
         if (!pool) return;
         for (auto& p : pieces)
             if (p.job) pool->wait(p.job.get());
@@ -624,6 +627,12 @@ struct HostIO {
         ck(cudaStreamWaitEvent(I.down_stream, ready, 0), "cudaStreamWaitEvent");
         copy2d((c_stage ? c_stage : C) + cr.off, result + cr.off, cr, cudaMemcpyDeviceToHost, I.down_stream, 4);
         I.last_down += cr.width * cr.height * 4;
+        if (tracing) {
+            cudaEvent_t e;
+            ck(cudaEventCreate(&e), "cudaEventCreate");
+            ck(cudaEventRecord(e, I.down_stream), "cudaEventRecord");
+            down_done.emplace_back(cr.width * cr.height * 4, e);
+        }
         if (c_stage) {
             downs.push_back(Down{cr, event(), nullptr});
             ck(cudaEventRecord(downs.back().ev, I.down_stream), "cudaEventRecord");
@@ -660,6 +669,8 @@ struct HostIO {
             const Piece& pc = pieces[j];
             std::fprintf(stderr, " %c%d%s%.3f", pc.which ? 'B' : 'A', pc.tag, pc.job ? "h" : "", at(ev_up[j]));
         }
+        std::fprintf(stderr, " | down");
+        for (const auto& d : down_done) std::fprintf(stderr, " %.1fM@%.3f", d.first / 1048576.0, at(d.second));
     }
 };
 
