@@ -375,6 +375,12 @@ int launch_impl(const TcGemmConfig& cfg, const TcGemmProblem& p, cudaStream_t st
                     std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 256,
                                  (i / 16) % 16, h[i], h[i + 1], h[i + 2], h[i + 3], h[i + 8], h[i + 9], h[i + 4], h[i + 5],
                                  h[i + 6], h[i + 10], h[i + 14], h[i + 7]);
+            // diagnostic builds (FI_TC_WAITPROF): MMA full-wait / loop cycles, producer
+            // empty-wait / loop cycles, K blocks
+            for (size_t i = 15 * 16; i < trace_n; i += 256)
+                if (h[i + 9] || h[i + 11])
+                    std::fprintf(f, "wait %zu %llu %llu %llu %llu %llu\n", i / 256, h[i + 8], h[i + 9], h[i + 10],
+                                 h[i + 11], h[i + 12]);
             std::fclose(f);
         }
     }

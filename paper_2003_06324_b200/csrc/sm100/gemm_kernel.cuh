@@ -36,6 +36,11 @@
 //    split_rank * kCtaGroup + pair_rank.
 #pragma once
 
+#ifndef FI_TC_WAITPROF
+#define FI_TC_WAITPROF 0  // diagnostic build: per-CTA barrier-wait cycles in trace row 15
+#endif
+
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -220,6 +225,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             const uint64_t pol_b = args.l2_hint == 1 ? kL2EvictFirst : args.l2_hint == 2 ? kL2EvictLast : kL2EvictNormal;
             UnitIter<BN> units(args, cluster, nclusters);
             Unit u;
+#if FI_TC_WAITPROF
+            long long w_empty = 0;
+            const long long t_loop = clock64();
+#endif
             while (units.next(u)) {
                 int tm, tn;
                 tile_coords(args, u.tile, tm, tn);
@@ -240,7 +249,15 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 const int n0 = tn * kBNTile + static_cast<int>(mc_rank) * S::BN_TILE + u.n_off +
                                static_cast<int>(pair_rank) * b_rows;
                 for (int kb = u.k0; kb < u.k1; kb += kKB) {
+#if FI_TC_WAITPROF
+                    {
+                        const long long t = clock64();
+                        mbar_wait(&empty_bar[s], ph ^ 1);
+                        w_empty += clock64() - t;
+                    }
+#else
                     mbar_wait(&empty_bar[s], ph ^ 1);
+#endif
                     uint8_t* sa = ring + s * S::STAGE_BYTES;
                     uint8_t* sb = sa + S::A_STAGE_BYTES;
                     const int k0 = (kb0 + kb) * S::BK;
@@ -312,6 +329,13 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     if (++s == nst) { s = 0; ph ^= 1; }
                 }
             }
+#if FI_TC_WAITPROF
+            if (issuer && args.trace) {
+                unsigned long long* row = args.trace + (blockIdx.x * 16 + 15) * 16;
+                row[10] = static_cast<unsigned long long>(w_empty);
+                row[11] = static_cast<unsigned long long>(clock64() - t_loop);
+            }
+#endif
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
@@ -334,6 +358,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             int it = 0;
             UnitIter<BN> units(args, cluster, nclusters);
             Unit u;
+#if FI_TC_WAITPROF
+            long long w_full = 0, n_kb = 0;
+            const long long t_loop = clock64();
+#endif
             while (units.next(u)) {
                 const int buf = S::kAccBufs == 2 ? (it & 1) : 0;
                 const uint32_t use = static_cast<uint32_t>(S::kAccBufs == 2 ? (it >> 1) : it);
@@ -344,7 +372,16 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 const uint32_t d_tmem = tmem_u + static_cast<uint32_t>(buf * S::ACC_COLS);
                 const uint32_t b_kb_bytes = static_cast<uint32_t>(u.width / kCtaGroup) * 128;  // B rows x 128 B
                 for (int kb = u.k0; kb < u.k1; kb += kKB) {
+#if FI_TC_WAITPROF
+                    {
+                        const long long t = clock64();
+                        mbar_wait(&full_bar[s], ph);
+                        w_full += clock64() - t;
+                        ++n_kb;
+                    }
+#else
                     mbar_wait(&full_bar[s], ph);
+#endif
                     tc_fence_after();
                     const uint32_t sa = smem_u32(ring + s * S::STAGE_BYTES);
                     const uint32_t sb = sa + S::A_STAGE_BYTES;
@@ -384,6 +421,14 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     trace_stamp(args, it - 1, 1);
                 }
             }
+#if FI_TC_WAITPROF
+            if (issuer && args.trace) {
+                unsigned long long* row = args.trace + (blockIdx.x * 16 + 15) * 16;
+                row[8] = static_cast<unsigned long long>(w_full);
+                row[9] = static_cast<unsigned long long>(clock64() - t_loop);
+                row[12] = static_cast<unsigned long long>(n_kb);
+            }
+#endif
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ epilogue

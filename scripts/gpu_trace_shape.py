@@ -1,5 +1,5 @@
 """Traced launches (FI_TC_TRACE) of tensor-core strategies after warm-up and an
-L2 flush. argv: out_prefix then one or more m,n,k,pair,tile_n,split[,multicast] specs."""
+L2 flush. argv: out_prefix then one or more m,n,k,pair,tile_n,split[,multicast[,stages]] specs."""
 import os, sys, torch
 sys.path.insert(0, ".")
 import paper_2003_06324_b200 as fi
@@ -8,7 +8,7 @@ prefix = sys.argv[1]
 for spec in sys.argv[2:]:
     m, n, k, pair, tn, sk, *mc = (int(x) for x in spec.split(","))
     plan = fi.Plan(fi.strategies.tc_strategy(m, n, k, pair=bool(pair), tile_n=tn, split_k=sk,
-                                             multicast=bool(mc and mc[0])))
+                                             multicast=bool(mc and mc[0]), stages=mc[1] if len(mc) > 1 else 0))
     A = torch.randn(m * k, device="cuda").half(); B = torch.randn(k * n, device="cuda").half()
     C = torch.empty(m * n, device="cuda")
     for _ in range(3): plan.launch(A.data_ptr(), B.data_ptr(), C.data_ptr(), s)

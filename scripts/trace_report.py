@@ -12,6 +12,8 @@ def main(path):
         if line.startswith("launch"):
             cur = {"hdr": line.strip(), "rows": []}
             launches.append(cur)
+        elif line.startswith("wait"):  # FI_TC_WAITPROF builds: cta full_wait mma_loop empty_wait prod_loop kb
+            cur.setdefault("wait", []).append([int(x) for x in line.split()[1:]])
         elif cur is not None:
             vals = [int(x) for x in line.split()]
             cur["rows"].append(tuple(vals[:6]))
@@ -65,6 +67,15 @@ def main(path):
                   f" max {max(ep) / 1e3 if ep else 0:6.2f}  (n={len(mm)})")
 
 
+    wt = last.get("wait")
+    if wt:
+        med = statistics.median
+        per_kb = [(w[2] / w[5], w[1] / w[5], w[4] / w[3] * w[5] / w[5]) for w in wt if w[5]]
+        print(f"wait profile (SM cycles, median over {len(wt)} CTAs): MMA loop {med([w[2] for w in wt if w[2]]):.0f}, "
+              f"of which waiting on full barriers {med([w[1] for w in wt if w[2]]):.0f}; producer loop "
+              f"{med([w[4] for w in wt if w[4]]):.0f}, waiting on empty barriers {med([w[3] for w in wt if w[4]]):.0f}; "
+              f"K blocks {med([w[5] for w in wt if w[5]]):.0f}; MMA loop per K block "
+              f"{med([x[0] for x in per_kb]):.0f}, full-wait per K block {med([x[1] for x in per_kb]):.0f}")
     fix = last.get("fix")
     if fix:
         pub = [(p - r) / 1e3 for r, p, _, _ in fix]
