@@ -5,9 +5,10 @@
 // (sm100/schedule.hpp: UnitIter, plan_schedule), so the checker exercises
 // exactly what the GPU runs.
 //
-// Model. Agents per simulated CTA: P (TMA producer thread), M (MMA issuer),
+// Model. Agents per simulated CTA: P and P2 (the two TMA producer warps, even and
+// odd ring stages), M (MMA issuer),
 // E (the four epilogue warps, which move in lockstep through named
-// barriers), and the asynchronous engines they drive: TMA (tensor loads), MMA
+// barriers), and the asynchronous engines they drive: TMA (tensor loads, one per producer), MMA
 // (tcgen05.mma, completion via tcgen05.commit), BR/BW (bulk and TMA stores:
 // their shared-memory reads and global writes complete separately,
 // cp.async.bulk.wait_group.read vs wait_group), G2S (bulk loads completing on
@@ -115,10 +116,12 @@ struct Flag {
     Clock clock;
 };
 
-enum Role { kP = 0, kM, kE, kTMA, kMMA, kBR, kBW, kG2S, kRoles };
+// kP / kTMA: producer warp 0 (even ring stages) and its loads; kP2 / kTMA2:
+// producer warp 3 (odd stages)
+enum Role { kP = 0, kM, kE, kTMA, kMMA, kBR, kBW, kG2S, kP2, kTMA2, kRoles };
 const char* role_name(int r) {
     static const char* n[] = {"producer", "mma-issuer", "epilogue", "tma-load", "tcgen05.mma", "bulk-read", "bulk-write",
-                              "bulk-load"};
+                              "bulk-load", "producer-2", "tma-load-2"};
     return n[r];
 }
 
@@ -174,7 +177,8 @@ public:
         std::vector<Task> tasks;
         for (int c = 0; c < ncl_; ++c)
             for (int r = 0; r < kRanks; ++r) {
-                tasks.push_back(producer(c, r));
+                tasks.push_back(producer(c, r, 0));
+                tasks.push_back(producer(c, r, 1));
                 tasks.push_back(mma(c, r));
                 tasks.push_back(epilogue(c, r));
             }
@@ -394,9 +398,10 @@ private:
     }
 
     // ------------------------------------------------------------------ roles
-    // warp 0: gemm_kernel.cuh "TMA producer"
-    Task producer(int cl, int rank) {
-        const int cta = cta_of(cl, rank), P = agent(cta, kP), T = agent(cta, kTMA);
+    // warps 0 and 3: gemm_kernel.cuh "TMA producers" -- warp pw fills the ring
+    // stages s with s % 2 == pw; both walk the same unit and stage sequence
+    Task producer(int cl, int rank, int pw) {
+        const int cta = cta_of(cl, rank), P = agent(cta, pw ? kP2 : kP), T = agent(cta, pw ? kTMA2 : kTMA);
         Cta& C = ctas_[static_cast<size_t>(cta)];
         int s = 0;
         uint32_t ph = 0;
@@ -426,6 +431,14 @@ private:
                 if (opt_.mutation != kMutGateSkipAcquire) join(vc_[static_cast<size_t>(P)], f.clock);
             }
             for (int kb = u.k0; kb < u.k1; ++kb) {
+                if ((s & 1) != pw) {  // the other producer's stage
+                    if (++s == nst_) {
+                        s = 0;
+                        ph ^= 1;
+                        ++lap;
+                    }
+                    continue;
+                }
                 if (opt_.mutation != kMutSkipEmptyWait) {
                     co_await wait(C.empty[static_cast<size_t>(s)], ph ^ 1);
                     acquire(P, C.empty[static_cast<size_t>(s)], ph ^ 1);

@@ -8,8 +8,9 @@
 //   load a sh {TMA_LOAD}  load b sh {TMA_LOAD}
 //   done                                   -> UMMA leaf (tcgen05.mma kind::f16)
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (leader CTA),
-// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM -> RF -> GL). The
+// Roles (256 threads): warps 0 and 3 = TMA producers (even / odd ring stages),
+// warp 1 = MMA issuer (leader CTA), warp 2 = TMEM allocator, warps 4..7 =
+// epilogue (TMEM -> RF -> GL). The
 // producer and MMA warps run their loops with all 32 lanes so every operand is
 // warp-uniform (uniform registers); one elected lane issues each TMA / MMA /
 // commit (elect.sync inside the asm) -- no per-issue waterfall, measured 3-16 %
@@ -210,12 +211,18 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     const int nclusters = gridDim.x / kClusterSize;
     const int kb0 = static_cast<int>(split_rank) * args.k_blocks;  // first K block of my slice
 
-    if (warp == 0) {
-        // ------------------------------------------------------------ TMA producer
-        // the whole warp runs the loop so every operand is warp-uniform (uniform
-        // registers, no per-issue waterfall); lane 0 issues
+    if (warp == 0 || warp == 3) {
+        // ------------------------------------------------------------ TMA producers
+        // Two warps share the ring: warp 0 fills the even stages, warp 3 the odd
+        // ones (each waits for its stage's empty barrier, credits the expected
+        // bytes and issues that stage's A and B loads). One warp issuing every
+        // load capped narrow tiles (N <= 128: 20-24 KB per K block) at ~400 SM
+        // cycles per K block, its loads queued behind each other; two issuers
+        // cut that 8-13 % (profiles/round2/ab_split_producer.log).
+        // Each warp runs its loop with all 32 lanes so every operand is warp-
+        // uniform (uniform registers, no per-issue waterfall); one lane issues.
         {
-            const bool issuer = lane == 0;
+            const bool issuer = lane == 0 && warp == 0;
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
@@ -249,6 +256,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 const int n0 = tn * kBNTile + static_cast<int>(mc_rank) * S::BN_TILE + u.n_off +
                                static_cast<int>(pair_rank) * b_rows;
                 for (int kb = u.k0; kb < u.k1; kb += kKB) {
+                    if ((warp == 0) != ((s & 1) == 0)) {  // the other producer's stage
+                        if (++s == nst) { s = 0; ph ^= 1; }
+                        continue;
+                    }
 #if FI_TC_WAITPROF
                     {
                         const long long t = clock64();
@@ -267,7 +278,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     if (mma_leader) mbar_arrive_expect_tx_warp(&full_bar[s], tx);
                     auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol) {
                         if (args.l2_hint) {
-                            if (!issuer) return;
+                            if (lane != 0) return;
                             if constexpr (kCtaGroup == 1) tma_load_2d_hint(dst, map, &full_bar[s], c0, c1, pol);
                             else tma_load_2d_pair_hint(dst, map, &full_bar[s], c0, c1, pol);
                         } else {
@@ -282,7 +293,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                     if constexpr (kMcast > 1) {
                         // my 64-row half of the A block, to me and my rank-twin in the other pair
                         const int h = static_cast<int>(mc_rank);
-                        if (!issuer) {
+                        if (lane != 0) {
                         } else if (args.a_mn_major)
                             tma_load_2d_pair_mc(sa + h * 8192, &tmA, &full_bar[s], m0 + h * 64, k0, mc_a_mask);
                         else  // tmA box: 64 K x 64 rows for multicast plans
@@ -296,7 +307,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                                 // one box for both K blocks: MN-major {64, 64, 2 panels, 2 K blocks},
                                 // K-major {64 k, 128 rows, 2 K blocks}
                                 if (args.a_mn_major) {
-                                    if (!issuer) {
+                                    if (lane != 0) {
                                     } else if constexpr (kCtaGroup == 1) tma_load_4d(sas, &tmA, &full_bar[s], 0, 0, m0s / 64, kb0 + kb);
                                     else tma_load_4d_pair(sas, &tmA, &full_bar[s], 0, 0, m0s / 64, kb0 + kb);
                                 } else {
