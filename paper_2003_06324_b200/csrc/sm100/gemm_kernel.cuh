@@ -364,6 +364,11 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
             //           K step of 16 = two atoms = 2KB.
             const uint32_t a_lbo = args.a_mn_major ? 8192 : 16, a_kstep = args.a_mn_major ? 2048 : 32;
             const uint32_t b_lbo = args.b_mn_major ? 8192 : 16, b_kstep = args.b_mn_major ? 2048 : 32;
+            // single-slab, single-N-half tiles issue a K block's four MMAs from one
+            // asm statement (umma_f16_kblock_warp): with two producers feeding the
+            // ring, the MMA warp's issue time bounds N = 64 tiles (~255 -> ~200 SM
+            // cycles per K block, profiles/round2/ab_kblock_mma_issue.log)
+            constexpr bool kWholeKBlock = kSlabs == 1 && kNHalves == 1 && S::BK == 64;
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
@@ -399,6 +404,15 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
 #pragma unroll
                     for (int b = 0; b < kKB; ++b) {
                         if (kKB > 1 && kb + b >= u.k1) break;  // a unit's odd last K block
+                        if constexpr (kWholeKBlock) {
+                            // the whole K block from one elected lane (see umma_f16_kblock_warp)
+                            const uint32_t acc = (kb > u.k0 || b > 0) ? 1u : 0u;
+                            umma_f16_kblock_warp<kCtaGroup>(
+                                d_tmem, static_cast<uint32_t>(smem_desc_sw128(sa + b * S::SLAB_BYTES, a_lbo, 1024)),
+                                a_kstep >> 4,
+                                static_cast<uint32_t>(smem_desc_sw128(sb + b * b_kb_bytes, b_lbo, 1024)),
+                                b_kstep >> 4, idesc, acc);
+                        } else {
 #pragma unroll
                         for (int k = 0; k < S::BK / 16; ++k) {
                             const uint32_t acc = (kb > u.k0 || b > 0 || k > 0) ? 1u : 0u;
@@ -420,6 +434,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                                     umma_f16_warp<kCtaGroup>(d_tmem + sl * BN, ad, bd, idesc, acc);
                                 }
                             }
+                        }
                         }
                     }
                     if constexpr (kCtaGroup == 1) umma_commit_warp(&empty_bar[s]);

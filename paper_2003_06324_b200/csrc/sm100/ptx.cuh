@@ -374,6 +374,38 @@ __device__ __forceinline__ void umma_f16_warp(uint32_t d_tmem, uint64_t adesc, u
             "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
     }
 }
+// One 64-deep K block (four K = 16 MMAs) from ONE elected lane in ONE asm
+// statement: the descriptors are assembled inside from their low words (start
+// address and LBO; the K step advances the start address by `a_inc` / `b_inc`
+// 16-byte units) and the constant high word of every SW128 descriptor here
+// (SBO 1024 B, version 1, 128B swizzle): one elect and fewer uniform-register
+// moves per K block than four umma_f16_warp calls.
+template <int kCtaGroup>
+__device__ __forceinline__ void umma_f16_kblock_warp(uint32_t d_tmem, uint32_t a_lo, uint32_t a_inc, uint32_t b_lo,
+                                                     uint32_t b_inc, uint32_t idesc, uint32_t accumulate) {
+#define FI_UMMA_KB(CG)                                                                    \
+    asm volatile(                                                                         \
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b32 hi, al, bl;\n\t.reg .b64 ad, bd;\n\t"        \
+        "elect.sync _|e, 0xffffffff;\n\t"                                                 \
+        "setp.ne.b32 p, %6, 0;\n\t"                                                       \
+        "setp.eq.b32 t, %6, %6;\n\t"                                                      \
+        "mov.b32 hi, 0x40004040;\n\t"                                                     \
+        "mov.b64 ad, {%1, hi};\n\tmov.b64 bd, {%3, hi};\n\t"                              \
+        "@e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], ad, bd, %5, p;\n\t"              \
+        "add.u32 al, %1, %2;\n\tadd.u32 bl, %3, %4;\n\t"                                  \
+        "mov.b64 ad, {al, hi};\n\tmov.b64 bd, {bl, hi};\n\t"                              \
+        "@e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], ad, bd, %5, t;\n\t"              \
+        "add.u32 al, al, %2;\n\tadd.u32 bl, bl, %4;\n\t"                                  \
+        "mov.b64 ad, {al, hi};\n\tmov.b64 bd, {bl, hi};\n\t"                              \
+        "@e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], ad, bd, %5, t;\n\t"              \
+        "add.u32 al, al, %2;\n\tadd.u32 bl, bl, %4;\n\t"                                  \
+        "mov.b64 ad, {al, hi};\n\tmov.b64 bd, {bl, hi};\n\t"                              \
+        "@e tcgen05.mma.cta_group::" CG ".kind::f16 [%0], ad, bd, %5, t;\n\t}"             \
+        ::"r"(d_tmem), "r"(a_lo), "r"(a_inc), "r"(b_lo), "r"(b_inc), "r"(idesc), "r"(accumulate))
+    if constexpr (kCtaGroup == 1) FI_UMMA_KB("1");
+    else FI_UMMA_KB("2");
+#undef FI_UMMA_KB
+}
 __device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
