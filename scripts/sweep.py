@@ -1,7 +1,10 @@
 #!/usr/bin/env python3
 """Config 4: shape sweep 256..8192 (square, tall-skinny, wide), several strategy
-trees per shape, one B200. Device time per launch (CUDA events, L2 flushed
-before every timed launch); writes profiles/<tag>_sweep.json and prints a table.
+trees per shape, one B200. Device time per launch with the L2 flushed before
+every launch: one CUDA-event pair around R x (flush + launch) minus one around
+R x flush, over R (single-launch event pairs step in ~2 us quanta on the B200
+box, profiles/round2/experiments.txt); median of `--steps` such sequences.
+Writes profiles/<tag>_sweep.json and prints a table.
 
   python scripts/sweep.py [--tag round1] [--quick]
 """
@@ -30,6 +33,30 @@ def peak():
         return 1590.0
 
 
+def per_launch_ms(fn, steps, flush, R=20):
+    """Median over `steps` of (R x (flush + fn) - R x flush) / R, in ms."""
+    s = torch.cuda.current_stream()
+
+    def seq(f):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(R):
+            flush.zero_()
+            if f:
+                f()
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    seq(fn)
+    ts = []
+    for _ in range(steps):
+        base = seq(None)
+        ts.append((seq(fn) - base) / R)
+    return statistics.median(ts)
+
+
 def time_plan(plan, steps, flush):
     m, n, k = plan.m, plan.n, plan.k
     (ar, ac, arow), (br, bc, brow), (cr, cc, crow) = plan.shapes()
@@ -40,16 +67,7 @@ def time_plan(plan, steps, flush):
     s = torch.cuda.current_stream()
     for _ in range(3):
         plan.launch(A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream)
-    ts = []
-    for _ in range(steps):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        plan.launch(A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream)
-        e1.record(s)
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    return statistics.median(ts)
+    return per_launch_ms(lambda: plan.launch(A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream), steps, flush)
 
 
 def time_cublas(m, n, k, steps, flush, out_dtype=torch.float32):
@@ -63,17 +81,7 @@ def time_cublas(m, n, k, steps, flush, out_dtype=torch.float32):
         f = lambda: torch.mm(b, a, out_dtype=out_dtype)
     for _ in range(3):
         f()
-    s = torch.cuda.current_stream()
-    ts = []
-    for _ in range(steps):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        f()
-        e1.record(s)
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    return statistics.median(ts)
+    return per_launch_ms(f, steps, flush)
 
 
 def candidates(m, n, k, quick):
@@ -89,7 +97,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", default="round1")
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     args = ap.parse_args()
     flush = torch.empty(128 << 20, device="cuda")
     pk = peak()
@@ -127,7 +135,9 @@ def main():
               flush=True)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{args.tag}_sweep.json"), "w") as f:
-        json.dump({"peak_tflops": pk, "l2": "flushed before every timed launch", "results": results}, f, indent=1)
+        json.dump({"peak_tflops": pk, "l2": "flushed before every timed launch",
+                   "timing": "per launch: (20 x (flush + launch) - 20 x flush) / 20, median of 5 sequences",
+                   "results": results}, f, indent=1)
 
 
 if __name__ == "__main__":
