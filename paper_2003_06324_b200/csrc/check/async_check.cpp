@@ -5,8 +5,8 @@
 // (sm100/schedule.hpp: UnitIter, plan_schedule), so the checker exercises
 // exactly what the GPU runs.
 //
-// Model. Agents per simulated CTA: P and P2 (the two TMA producer warps, even and
-// odd ring stages), M (MMA issuer),
+// Model. Agents per simulated CTA: P, P2, P3 (the three TMA producer warps, ring
+// stages s % 3 = 0, 1, 2), M (MMA issuer),
 // E (the four epilogue warps, which move in lockstep through named
 // barriers), and the asynchronous engines they drive: TMA (tensor loads, one per producer), MMA
 // (tcgen05.mma, completion via tcgen05.commit), BR/BW (bulk and TMA stores:
@@ -116,12 +116,12 @@ struct Flag {
     Clock clock;
 };
 
-// kP / kTMA: producer warp 0 (even ring stages) and its loads; kP2 / kTMA2:
-// producer warp 3 (odd stages)
-enum Role { kP = 0, kM, kE, kTMA, kMMA, kBR, kBW, kG2S, kP2, kTMA2, kRoles };
+// kP / kTMA, kP2 / kTMA2, kP3 / kTMA3: the three producer warps (ring stages
+// s % 3 = 0, 1, 2) and their loads
+enum Role { kP = 0, kM, kE, kTMA, kMMA, kBR, kBW, kG2S, kP2, kTMA2, kP3, kTMA3, kRoles };
 const char* role_name(int r) {
-    static const char* n[] = {"producer", "mma-issuer", "epilogue", "tma-load", "tcgen05.mma", "bulk-read", "bulk-write",
-                              "bulk-load", "producer-2", "tma-load-2"};
+    static const char* n[] = {"producer", "mma-issuer", "epilogue",   "tma-load",   "tcgen05.mma", "bulk-read",
+                              "bulk-write", "bulk-load", "producer-2", "tma-load-2", "producer-3",  "tma-load-3"};
     return n[r];
 }
 
@@ -177,8 +177,7 @@ public:
         std::vector<Task> tasks;
         for (int c = 0; c < ncl_; ++c)
             for (int r = 0; r < kRanks; ++r) {
-                tasks.push_back(producer(c, r, 0));
-                tasks.push_back(producer(c, r, 1));
+                for (int pw = 0; pw < 3; ++pw) tasks.push_back(producer(c, r, pw));
                 tasks.push_back(mma(c, r));
                 tasks.push_back(epilogue(c, r));
             }
@@ -398,10 +397,11 @@ private:
     }
 
     // ------------------------------------------------------------------ roles
-    // warps 0 and 3: gemm_kernel.cuh "TMA producers" -- warp pw fills the ring
-    // stages s with s % 2 == pw; both walk the same unit and stage sequence
+    // warps 0, 3, 2: gemm_kernel.cuh "TMA producers" -- producer pw fills the
+    // ring stages s with s % 3 == pw; all walk the same unit and stage sequence
     Task producer(int cl, int rank, int pw) {
-        const int cta = cta_of(cl, rank), P = agent(cta, pw ? kP2 : kP), T = agent(cta, pw ? kTMA2 : kTMA);
+        const int cta = cta_of(cl, rank), P = agent(cta, pw == 0 ? kP : pw == 1 ? kP2 : kP3),
+                  T = agent(cta, pw == 0 ? kTMA : pw == 1 ? kTMA2 : kTMA3);
         Cta& C = ctas_[static_cast<size_t>(cta)];
         int s = 0;
         uint32_t ph = 0;
@@ -431,7 +431,7 @@ private:
                 if (opt_.mutation != kMutGateSkipAcquire) join(vc_[static_cast<size_t>(P)], f.clock);
             }
             for (int kb = u.k0; kb < u.k1; ++kb) {
-                if ((s & 1) != pw) {  // the other producer's stage
+                if (s % 3 != pw) {  // another producer's stage
                     if (++s == nst_) {
                         s = 0;
                         ph ^= 1;

@@ -8,9 +8,9 @@
 //   load a sh {TMA_LOAD}  load b sh {TMA_LOAD}
 //   done                                   -> UMMA leaf (tcgen05.mma kind::f16)
 //
-// Roles (256 threads): warps 0 and 3 = TMA producers (even / odd ring stages),
-// warp 1 = MMA issuer (leader CTA), warp 2 = TMEM allocator, warps 4..7 =
-// epilogue (TMEM -> RF -> GL). The
+// Roles (256 threads): warps 0, 3 and 2 = TMA producers (ring stages s % 3 =
+// 0, 1, 2), warp 1 = MMA issuer (leader CTA), warp 2 also allocates TMEM,
+// warps 4..7 = epilogue (TMEM -> RF -> GL). The
 // producer and MMA warps run their loops with all 32 lanes so every operand is
 // warp-uniform (uniform registers); one elected lane issues each TMA / MMA /
 // commit (elect.sync inside the asm) -- no per-issue waterfall, measured 3-16 %
@@ -211,14 +211,16 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     const int nclusters = gridDim.x / kClusterSize;
     const int kb0 = static_cast<int>(split_rank) * args.k_blocks;  // first K block of my slice
 
-    if (warp == 0 || warp == 3) {
+    if (warp == 0 || warp == 2 || warp == 3) {
         // ------------------------------------------------------------ TMA producers
-        // Two warps share the ring: warp 0 fills the even stages, warp 3 the odd
-        // ones (each waits for its stage's empty barrier, credits the expected
-        // bytes and issues that stage's A and B loads). One warp issuing every
-        // load capped narrow tiles (N <= 128: 20-24 KB per K block) at ~400 SM
-        // cycles per K block, its loads queued behind each other; two issuers
-        // cut that 8-13 % (profiles/round2/ab_split_producer.log).
+        // Three warps share the ring: stage s is filled by warp 0, 3 or 2 for
+        // s % 3 = 0, 1, 2 (each waits for its stage's empty barrier, credits the
+        // expected bytes and issues that stage's A and B loads; warp 2 allocated
+        // TMEM before the prologue sync). A warp spends ~500 SM cycles per stage
+        // issuing its loads (FI_TC_WAITPROF builds), so one producer capped narrow
+        // tiles (N <= 128: 20-24 KB per K block) at ~400 cycles per K block; two
+        // and then three issuers cut that to ~295 (profiles/round2/ab_split_producer.log,
+        // ab_three_producers.log).
         // Each warp runs its loop with all 32 lanes so every operand is warp-
         // uniform (uniform registers, no per-issue waterfall); one lane issues.
         {
@@ -256,7 +258,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 const int n0 = tn * kBNTile + static_cast<int>(mc_rank) * S::BN_TILE + u.n_off +
                                static_cast<int>(pair_rank) * b_rows;
                 for (int kb = u.k0; kb < u.k1; kb += kKB) {
-                    if ((warp == 0) != ((s & 1) == 0)) {  // the other producer's stage
+                    if (warp != (s % 3 == 0 ? 0 : s % 3 == 1 ? 3 : 2)) {  // another producer's stage
                         if (++s == nst) { s = 0; ph ^= 1; }
                         continue;
                     }
