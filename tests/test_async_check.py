@@ -151,3 +151,13 @@ def test_multicast_pairs_are_race_free(fi, tc, tn, shape, layouts):
         pytest.skip("N must hold two tiles")
     r = fi.check_async(tc(*shape, tile_n=tn, multicast=True, layouts=layouts))
     assert r.ok and r.cluster_size == 4 and r.mode == 0, r.text
+
+
+# three producer warps over ring depths that are and are not multiples of three
+# (the GPU side: tests/test_gpu_tc.py::test_ring_depths_with_three_producers)
+@pytest.mark.parametrize("stages", [2, 3, 4, 5, 7])
+@pytest.mark.parametrize("kw", [dict(pair=False, tile_n=64), dict(pair=True, tile_n=128),
+                                dict(pair=True, tile_n=64, multicast=True)], ids=["cta64", "pair128", "pair64_mcast"])
+def test_three_producers_any_ring_depth(fi, tc, stages, kw):
+    r = fi.check_async(tc(1024, 512, 1472, stages=stages, **kw))
+    assert r.ok and r.stages == stages, r.text

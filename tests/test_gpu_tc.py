@@ -315,3 +315,17 @@ def test_f16_ingestion_saturates_like_round_to_f16(fi, oracle):
     want = oracle.round_elem(a, "f16")
     assert np.isfinite(c).all()
     assert np.array_equal(c, want)
+
+
+# Three producer warps fill the ring stages s % 3 = 0, 1, 2 (gemm_kernel.cuh); ring
+# depths that are and are not multiples of three, and shallower than three, must
+# all give the exact result -- over units that wrap the ring several times.
+@pytest.mark.parametrize("stages", [2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("cfg", [dict(pair=False, tile_n=64), dict(pair=True, tile_n=128),
+                                 dict(pair=True, tile_n=64, multicast=True), dict(pair=True, tile_n=256, tile_m=512)],
+                         ids=["cta64", "pair128", "pair64_mcast", "slab512"])
+def test_ring_depths_with_three_producers(fi, oracle, stages, cfg):
+    m, n, k = 1024, 512, 1472  # 23 K blocks per tile: not a multiple of any ring depth
+    s = fi.strategies.tc_strategy(m, n, k, stages=stages, **cfg)
+    c, ar, br = run(fi, oracle, s, m, n, k, True, seed=11 + stages)
+    assert np.array_equal(c, oracle.gemm_f64(ar, br))
