@@ -135,6 +135,7 @@ class Checker {
     static constexpr int NCH_ALL = NCH * kSlabs * kNHalves;  // 32-column chunks of a tile's CTA rows, all accumulators
     static constexpr int kChunkBytes = 32 * S::BM * 4;
     static constexpr int kGran = 1024;  // shared-memory cell granularity (bytes)
+    static constexpr int kProducers = kSlabs * kNHalves > 1 ? 1 : 3;  // as gemm_kernel.cuh
 
 public:
     Checker(const GemmArgs& args, int clusters, long slots, const AsyncCheckOptions& o, AsyncReport& rep)
@@ -177,7 +178,7 @@ public:
         std::vector<Task> tasks;
         for (int c = 0; c < ncl_; ++c)
             for (int r = 0; r < kRanks; ++r) {
-                for (int pw = 0; pw < 3; ++pw) tasks.push_back(producer(c, r, pw));
+                for (int pw = 0; pw < kProducers; ++pw) tasks.push_back(producer(c, r, pw));
                 tasks.push_back(mma(c, r));
                 tasks.push_back(epilogue(c, r));
             }
@@ -431,7 +432,7 @@ private:
                 if (opt_.mutation != kMutGateSkipAcquire) join(vc_[static_cast<size_t>(P)], f.clock);
             }
             for (int kb = u.k0; kb < u.k1; ++kb) {
-                if (s % 3 != pw) {  // another producer's stage
+                if (s % kProducers != pw) {  // another producer's stage
                     if (++s == nst_) {
                         s = 0;
                         ph ^= 1;

@@ -211,7 +211,11 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
     const int nclusters = gridDim.x / kClusterSize;
     const int kb0 = static_cast<int>(split_rank) * args.k_blocks;  // first K block of my slice
 
-    if (warp == 0 || warp == 2 || warp == 3) {
+    // wide tiles (two A slabs or two B halves per stage: 48 KB, 4 stages) keep one
+    // producer -- three cost them 1-7 % (stages issued out of order), and their
+    // MMA work per stage hides one warp's issue time (ab_three_producers.log)
+    constexpr int kProducers = kSlabs * kNHalves > 1 ? 1 : 3;
+    if (warp == 0 || (kProducers == 3 && (warp == 2 || warp == 3))) {
         // ------------------------------------------------------------ TMA producers
         // Three warps share the ring: stage s is filled by warp 0, 3 or 2 for
         // s % 3 = 0, 1, 2 (each waits for its stage's empty barrier, credits the
@@ -258,7 +262,7 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
                 const int n0 = tn * kBNTile + static_cast<int>(mc_rank) * S::BN_TILE + u.n_off +
                                static_cast<int>(pair_rank) * b_rows;
                 for (int kb = u.k0; kb < u.k1; kb += kKB) {
-                    if (warp != (s % 3 == 0 ? 0 : s % 3 == 1 ? 3 : 2)) {  // another producer's stage
+                    if (kProducers == 3 && warp != (s % 3 == 0 ? 0 : s % 3 == 1 ? 3 : 2)) {  // another producer's stage
                         if (++s == nst) { s = 0; ph ^= 1; }
                         continue;
                     }
