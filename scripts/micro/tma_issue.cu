@@ -124,6 +124,30 @@ __global__ void __launch_bounds__(128, 1) k3(const __grid_constant__ CUtensorMap
     }
 }
 
+// issue loop with the tensor map read from global memory (pointer) instead of
+// the kernel-parameter copy: loads only, 1 or 3 warps
+__global__ void __launch_bounds__(128, 1) k4(const CUtensorMap* tmg, int bytes, int iters, int nwarps, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* ring = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + kStages * kStage);
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        fence_barrier_init();
+        tma_prefetch_desc(tmg);
+    }
+    __syncthreads();
+    long long t0 = clock64();
+    if (warp < nwarps) {
+        int s = 0;
+        for (int i = 0; i < iters; ++i) {
+            if (i % nwarps == warp) tma_load_2d_warp(ring + s * kStage, tmg, &full[s], 0, (i * (bytes / 128)) % 8192);
+            if (++s == kStages) s = 0;
+        }
+        if ((threadIdx.x & 31) == 0) out[1 + warp] = clock64() - t0;
+    }
+}
+
 // latency: one warp, one load in flight
 __global__ void __launch_bounds__(128, 1) k2(const __grid_constant__ CUtensorMap tm, int bytes, int iters, long long* out) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -170,6 +194,7 @@ int main() {
     cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     // box-size sweep with 3 issuing warps: one load per fill of rows x 128 B (4..32 KB)
     for (int rows : {32, 64, 128, 256}) {
         CUtensorMap tr;
@@ -204,6 +229,24 @@ int main() {
                 std::printf("%d warp(s), 16 KB fills, %-28s: issue loop %5.0f cycles per fill%s\n", nw, names[mode],
                             double(h[1]) / 512, e == cudaSuccess ? "" : cudaGetErrorString(e));
             }
+        }
+    }
+    {
+        CUtensorMap tr;
+        cuuint32_t box[2] = {64, 128};
+        encode(&tr, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, A, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        CUtensorMap* tg;
+        cudaMalloc(&tg, sizeof(CUtensorMap));
+        cudaMemcpy(tg, &tr, sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+        for (int nw : {1, 3}) {
+            cudaMemset(d, 0, 8 * sizeof(long long));
+            k4<<<1, 128, smem>>>(tg, 16384, 512, nw, d);
+            cudaError_t e = cudaDeviceSynchronize();
+            long long h[8];
+            cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+            std::printf("%d warp(s), 16 KB fills, load only, tensor map in global memory: issue loop %5.0f cycles per fill%s\n",
+                        nw, double(h[1]) / 512, e == cudaSuccess ? "" : cudaGetErrorString(e));
         }
     }
     // latency: one load in flight at a time (issue, wait for it to land, repeat)
