@@ -378,8 +378,9 @@ __device__ __forceinline__ void umma_f16_warp(uint32_t d_tmem, uint64_t adesc, u
 // statement: the descriptors are assembled inside from their low words (start
 // address and LBO; the K step advances the start address by `a_inc` / `b_inc`
 // 16-byte units) and the constant high word of every SW128 descriptor here
-// (SBO 1024 B, version 1, 128B swizzle): one elect and fewer uniform-register
-// moves per K block than four umma_f16_warp calls.
+// (SBO 1024 B, version 1, 128B swizzle: kSw128DescHiSbo1024, checked against
+// smem_desc_sw128 below): one elect and fewer uniform-register moves per K block
+// than four umma_f16_warp calls.
 template <int kCtaGroup>
 __device__ __forceinline__ void umma_f16_kblock_warp(uint32_t d_tmem, uint32_t a_lo, uint32_t a_inc, uint32_t b_lo,
                                                      uint32_t b_inc, uint32_t idesc, uint32_t accumulate) {
@@ -524,6 +525,11 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t cluster_addr) {
 // ---------------------------------------------------------------- descriptors
 // UMMA shared-memory matrix descriptor, 128B swizzle (layout type 2), sm_100
 // version bit set. Address/offset fields are in 16-byte units.
+// High word of smem_desc_sw128(addr, lbo, 1024): SBO 1024 B, descriptor version 1,
+// 128B swizzle -- the constant umma_f16_kblock_warp assembles its descriptors with.
+constexpr uint32_t kSw128DescHiSbo1024 = (1024u >> 4) | (1u << 14) | (2u << 29);
+static_assert(kSw128DescHiSbo1024 == 0x40004040u, "umma_f16_kblock_warp's descriptor high word");
+
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo_bytes,
                                                     uint32_t sbo_bytes) {
     uint64_t d = 0;
