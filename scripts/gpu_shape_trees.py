@@ -10,6 +10,8 @@ from scripts.sweep import per_launch_ms
 TREES = {
     "pair256": dict(pair=True, tile_n=256), "pair256_mcast": dict(pair=True, tile_n=256, multicast=True),
     "pair128": dict(pair=True, tile_n=128), "pair128_mcast": dict(pair=True, tile_n=128, multicast=True),
+    "pair64": dict(pair=True, tile_n=64), "pair64_mcast": dict(pair=True, tile_n=64, multicast=True),
+    "cta64": dict(pair=False, tile_n=64),
     "slab512": dict(pair=True, tile_n=256, tile_m=512), "nhalf512": dict(pair=True, tile_n=512),
     "cta256": dict(pair=False, tile_n=256), "cta128": dict(pair=False, tile_n=128),
 }
