@@ -50,9 +50,12 @@ def draw(rng):
     return m, n, k, kw
 
 
+# FI_FUZZ_CASES / FI_FUZZ_SEED widen a one-off stress run (defaults: the fixed 80)
+import os  # noqa: E402
+
 CASES = []
-_rng = np.random.default_rng(20261017)
-while len(CASES) < 80:
+_rng = np.random.default_rng(int(os.environ.get("FI_FUZZ_SEED", "20261017")))
+while len(CASES) < int(os.environ.get("FI_FUZZ_CASES", "80")):
     CASES.append(draw(_rng))
 
 
