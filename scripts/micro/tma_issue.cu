@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <vector>
 
 #include "../../paper_2003_06324_b200/csrc/sm100/ptx.cuh"
@@ -122,6 +123,10 @@ __global__ void __launch_bounds__(128, 1) k3(const __grid_constant__ CUtensorMap
         }
         if ((threadIdx.x & 31) == 0) out[1 + warp] = clock64() - t0;
     }
+    // loads issued without a barrier to wait on must land before the CTA exits
+    const long long te = clock64();
+    while (clock64() - te < 200000) {
+    }
 }
 
 // issue loop with the tensor map read from global memory (pointer) instead of
@@ -146,6 +151,48 @@ __global__ void __launch_bounds__(128, 1) k4(const CUtensorMap* tmg, int bytes, 
         }
         if ((threadIdx.x & 31) == 0) out[1 + warp] = clock64() - t0;
     }
+    const long long te = clock64();  // let the unawaited loads land before exit
+    while (clock64() - te < 200000) {
+    }
+}
+
+// two CTAs per SM: each CTA runs its own 4-stage ring of 24 KB fills (A 16 KB +
+// B 8 KB boxes) with 3 issuing warps; per-CTA cycles per fill, grid 148 vs 296
+__global__ void __launch_bounds__(128, 2) k5(const __grid_constant__ CUtensorMap tmA,
+                                             const __grid_constant__ CUtensorMap tmB, int iters, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    constexpr int kS = 3;  // warp w owns stage w (one owner per stage: no parity ambiguity)
+    uint8_t* ring = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + kS * kStage);
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kS; ++s) mbar_init(&full[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    long long t0 = clock64();
+    if (warp < 3) {
+        uint32_t ph = 0;
+        int s = 0;
+        for (int i = 0; i < iters; ++i) {
+            if (s == warp) {
+                if (i >= kS) mbar_wait(&full[s], ph ^ 1);
+                mbar_arrive_expect_tx_warp(&full[s], kStage);
+                const int row = (blockIdx.x * 37 + i) * 128 % 8192;
+                tma_load_2d_warp(ring + s * kStage, &tmA, &full[s], 0, row);
+                tma_load_2d_warp(ring + s * kStage + kA, &tmB, &full[s], 0, row / 2);
+            }
+            if (++s == kS) { s = 0; ph ^= 1; }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kS && s < iters; ++s) {
+            const int last = ((iters - 1 - s) / kS) * kS + s;
+            mbar_wait(&full[s], static_cast<uint32_t>((last / kS) & 1));
+        }
+        out[blockIdx.x] = clock64() - t0;
+    }
 }
 
 // latency: one warp, one load in flight
@@ -169,7 +216,8 @@ __global__ void __launch_bounds__(128, 1) k2(const __grid_constant__ CUtensorMap
     }
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const bool only_k5 = argc > 1;
     using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -197,6 +245,7 @@ int main() {
     cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     // box-size sweep with 3 issuing warps: one load per fill of rows x 128 B (4..32 KB)
     for (int rows : {32, 64, 128, 256}) {
+        if (only_k5) break;
         CUtensorMap tr;
         cuuint32_t box[2] = {64, static_cast<cuuint32_t>(rows)};
         encode(&tr, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, A, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -220,6 +269,7 @@ int main() {
         const char* names[] = {"wait + expect_tx + load", "expect_tx + load (no wait)", "load only",
                                "wait + arrive (no load)"};
         for (int nw : {1, 3}) {
+            if (only_k5) break;
             for (int mode = 0; mode < 4; ++mode) {
                 cudaMemset(d, 0, 8 * sizeof(long long));
                 k3<<<1, 128, smem>>>(tr, 16384, 512, nw, mode, d);
@@ -240,6 +290,7 @@ int main() {
         cudaMalloc(&tg, sizeof(CUtensorMap));
         cudaMemcpy(tg, &tr, sizeof(CUtensorMap), cudaMemcpyHostToDevice);
         for (int nw : {1, 3}) {
+            if (only_k5) break;
             cudaMemset(d, 0, 8 * sizeof(long long));
             k4<<<1, 128, smem>>>(tg, 16384, 512, nw, d);
             cudaError_t e = cudaDeviceSynchronize();
@@ -247,6 +298,25 @@ int main() {
             cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
             std::printf("%d warp(s), 16 KB fills, load only, tensor map in global memory: issue loop %5.0f cycles per fill%s\n",
                         nw, double(h[1]) / 512, e == cudaSuccess ? "" : cudaGetErrorString(e));
+        }
+    }
+    {
+        const int smem5 = 3 * kStage + 1024 + 256;
+        cudaFuncSetAttribute(k5, cudaFuncAttributeMaxDynamicSharedMemorySize, smem5);
+        long long* d5;
+        cudaMalloc(&d5, 296 * sizeof(long long));
+        for (int grid : {148, 296}) {
+            for (int rep = 0; rep < 2; ++rep) {
+                k5<<<grid, 128, smem5>>>(ta, tb, 512, d5);
+                cudaError_t e = cudaDeviceSynchronize();
+                std::vector<long long> h(grid);
+                cudaMemcpy(h.data(), d5, grid * sizeof(long long), cudaMemcpyDeviceToHost);
+                std::sort(h.begin(), h.end());
+                if (rep)
+                    std::printf("grid %d (3-stage ring, 24 KB fills, 3 warps per CTA): median %5.0f cycles per fill per CTA"
+                                " -> %.1f B/clk per SM%s\n", grid, double(h[grid / 2]) / 512,
+                                (grid / 148) * 512.0 * kStage / h[grid / 2], e == cudaSuccess ? "" : cudaGetErrorString(e));
+            }
         }
     }
     // latency: one load in flight at a time (issue, wait for it to land, repeat)
