@@ -29,15 +29,17 @@ __global__ void k_small(int* out) {
 __global__ void k_big(const __grid_constant__ Params p, int* out) {
     if (threadIdx.x == 0 && blockIdx.x == 0 && out) out[0] = p.args[0] + p.m[4].b[3];
 }
+// variant bits: 1 relinquish the allocation permit, 2 dealloc at the end
+template <int kVariant>
 __global__ void k_tmem(int* out) {
     __shared__ uint32_t slot;
     if (threadIdx.x < 32) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
             static_cast<uint32_t>(__cvta_generic_to_shared(&slot))));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (kVariant & 1) asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     __syncthreads();
-    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(slot));
+    if ((kVariant & 2) && threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(slot));
     if (threadIdx.x == 0 && blockIdx.x == 0 && out) out[0] = 1;
 }
 
@@ -47,7 +49,8 @@ int main() {
     void* flush;
     const size_t fb = 128u << 20;
     cudaMalloc(&flush, fb);
-    for (auto f : {(const void*)k_small, (const void*)k_big, (const void*)k_tmem})
+    for (auto f : {(const void*)k_small, (const void*)k_big, (const void*)k_tmem<3>, (const void*)k_tmem<2>,
+                   (const void*)k_tmem<1>, (const void*)k_tmem<0>})
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaStream_t s;
     cudaStreamCreate(&s);
@@ -57,7 +60,7 @@ int main() {
     Params P{};
     struct Cfg {
         const char* name;
-        int kind;  // 0 small, 1 big params, 2 tmem
+        int kind;  // 0 small, 1 big params, 2 tmem alloc+relinquish+dealloc, 3 alloc+dealloc, 4 alloc+relinquish, 5 alloc only
         int smem, cluster;
         bool coop;
         int grid, launches;
@@ -70,7 +73,10 @@ int main() {
         {"cluster 2", 0, 0, 2, false, 148, 1},
         {"coop", 0, 0, 1, true, 148, 1},
         {"big params", 1, 0, 1, false, 148, 1},
-        {"tmem alloc/dealloc", 2, 0, 1, false, 148, 1},
+        {"tmem alloc + relinquish + dealloc", 2, 0, 1, false, 148, 1},
+        {"tmem alloc + dealloc", 3, 0, 1, false, 148, 1},
+        {"tmem alloc + relinquish (no dealloc)", 4, 0, 1, false, 148, 1},
+        {"tmem alloc only", 5, 0, 1, false, 148, 1},
         {"smem 227K + coop", 0, 227 * 1024, 1, true, 148, 1},
         {"big params + smem + coop", 1, 227 * 1024, 1, true, 148, 1},
         {"big params + cluster 2 + smem + coop", 1, 227 * 1024, 2, true, 148, 1},
@@ -108,7 +114,10 @@ int main() {
                 lc.attrs = at;
                 lc.numAttrs = na;
                 cudaError_t err = c->kind == 1   ? cudaLaunchKernelEx(&lc, k_big, P, d)
-                                  : c->kind == 2 ? cudaLaunchKernelEx(&lc, k_tmem, d)
+                                  : c->kind == 2 ? cudaLaunchKernelEx(&lc, k_tmem<3>, d)
+                                  : c->kind == 3 ? cudaLaunchKernelEx(&lc, k_tmem<2>, d)
+                                  : c->kind == 4 ? cudaLaunchKernelEx(&lc, k_tmem<1>, d)
+                                  : c->kind == 5 ? cudaLaunchKernelEx(&lc, k_tmem<0>, d)
                                                  : cudaLaunchKernelEx(&lc, k_small, d);
                 if (err != cudaSuccess) {
                     std::printf("%s: %s\n", c->name, cudaGetErrorString(err));
