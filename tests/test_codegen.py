@@ -111,3 +111,23 @@ def test_generic_sources_compile_with_nvrtc(fi, key):
         script = golden_script(key)
     ok, log = _nvrtc_compile(fi.generate(script))
     assert ok, log
+
+
+def test_wait_profile_diagnostic_build_compiles(tmp_path):
+    """The diagnostic build (-DFI_TC_WAITPROF=1) of one kernel
+    instantiation still compiles for sm_100a and keeps the three producer warps'
+    TMA issue and the single-asm K block (UTMALDG, UTCHMMA in the SASS)."""
+    root = os.path.join(os.path.dirname(__file__), "..", "paper_2003_06324_b200", "csrc")
+    src = tmp_path / "waitprof.cu"
+    src.write_text('#include "sm100/gemm_kernel.cuh"\n'
+                   "template __global__ void fireiron::sm100::fi_sm100_gemm<1, 64, 1, 1, 1>(\n"
+                   "    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,\n"
+                   "    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,\n"
+                   "    const __grid_constant__ CUtensorMap, const __grid_constant__ fireiron::sm100::GemmArgs);\n")
+    cubin = tmp_path / "waitprof.cubin"
+    r = subprocess.run([NVCC, "-cubin", "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "-O2",
+                        "-DFI_TC_WAITPROF=1", "-I", root, "-I", os.path.join(root, "..", "..", "include"),
+                        "-o", str(cubin), str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    sass = subprocess.run(["cuobjdump", "-sass", str(cubin)], capture_output=True, text=True).stdout
+    assert "UTMALDG" in sass and "UTCHMMA" in sass and "CS2R" in sass  # clock reads of the wait profile
