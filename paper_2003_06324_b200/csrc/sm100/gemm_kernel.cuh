@@ -224,7 +224,10 @@ __device__ __forceinline__ void fi_sm100_gemm_body(const CUtensorMap& tmA, const
         // issuing its loads (FI_TC_WAITPROF builds), so one producer capped narrow
         // tiles (N <= 128: 20-24 KB per K block) at ~400 cycles per K block; two
         // and then three issuers cut that to ~295 (profiles/round2/ab_split_producer.log,
-        // ab_three_producers.log).
+        // ab_three_producers.log). A stage always has the same producer, so no
+        // producer can get two fills ahead of a stage's empty barrier and pass its
+        // parity wait on a stale phase (ownership by fill count instead broke that
+        // with shallow rings -- the CPU protocol checker's find, experiments.txt).
         // Each warp runs its loop with all 32 lanes so every operand is warp-
         // uniform (uniform registers, no per-issue waterfall); one lane issues.
         {
