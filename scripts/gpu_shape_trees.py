@@ -12,6 +12,7 @@ TREES = {
     "pair128": dict(pair=True, tile_n=128), "pair128_mcast": dict(pair=True, tile_n=128, multicast=True),
     "pair64": dict(pair=True, tile_n=64), "pair64_mcast": dict(pair=True, tile_n=64, multicast=True),
     "cta64": dict(pair=False, tile_n=64),
+    "pair256_s5": dict(pair=True, tile_n=256, stages=5), "pair256_s4": dict(pair=True, tile_n=256, stages=4),
     "slab512": dict(pair=True, tile_n=256, tile_m=512), "nhalf512": dict(pair=True, tile_n=512),
     "cta256": dict(pair=False, tile_n=256), "cta128": dict(pair=False, tile_n=128),
 }
