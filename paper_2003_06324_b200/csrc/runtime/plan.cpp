@@ -933,13 +933,21 @@ std::shared_ptr<Plan> Plan::create(const Spec& root, const NodePtr& tree, const 
         c.b_mn_major = mm.b.layout.major == Major::RowMajor ? 1 : 0;
         c.c_row_major = mm.c.layout.major == Major::RowMajor ? 1 : 0;
         c.out_type = elem_code(mm.c.elem);
-        c.group_m = 8;
-        if (const char* e = std::getenv("FI_TC_GROUP_M")) c.group_m = std::atoi(e);  // raster band (experiments)
         c.stages = tc.stages;
         c.slabs = tc.tile_m / (128 * tc.cta_group);
         c.n_halves = tc.tile_n == 512 ? 2 : 1;  // two N = 256 MMAs sharing A
         c.mcast = tc.mcast;
         c.bn = tc.tile_n / c.n_halves;
+        // raster band: 8 tile rows; 256 x 256 pair tiles whose whole A fits in a
+        // third of L2 (<= 48 MiB) sweep it column by column instead (one band of
+        // every tile row): C2 4096^3 +0.9 %, 4096 x 8192 x 4096 +2-5 %; narrow
+        // 1-CTA tiles on tall shapes lose 5-8 % that way, so they keep 8
+        // (profiles/round2/ab_group_m.log)
+        c.group_m = 8;
+        if (c.cta_group == 2 && c.bn == 256 && c.slabs == 1 && c.n_halves == 1 && c.mcast == 1 &&
+            static_cast<double>(root.m()) * root.k() * 2.0 <= 48.0 * (1 << 20))
+            c.group_m = static_cast<int>(root.m() / 256);
+        if (const char* e = std::getenv("FI_TC_GROUP_M")) c.group_m = std::atoi(e);  // raster band (experiments)
         if (sm100::tc_gemm_check(c, static_cast<int>(root.m()), static_cast<int>(root.n()),
                                  static_cast<int>(root.k())) != sm100::kTcOk)
             throw BackendError(103, "no tcgen05 kernel instance for this tile configuration");
