@@ -13,6 +13,8 @@ TREES = {
     "pair64": dict(pair=True, tile_n=64), "pair64_mcast": dict(pair=True, tile_n=64, multicast=True),
     "cta64": dict(pair=False, tile_n=64),
     "pair256_s5": dict(pair=True, tile_n=256, stages=5), "pair256_s4": dict(pair=True, tile_n=256, stages=4),
+    "pair256_sk2": dict(pair=True, tile_n=256, split_k=2), "pair256_sk4": dict(pair=True, tile_n=256, split_k=4),
+    "pair256_sk8": dict(pair=True, tile_n=256, split_k=8), "pair128_sk4": dict(pair=True, tile_n=128, split_k=4),
     "slab512": dict(pair=True, tile_n=256, tile_m=512), "nhalf512": dict(pair=True, tile_n=512),
     "cta256": dict(pair=False, tile_n=256), "cta128": dict(pair=False, tile_n=128),
 }
